@@ -1,0 +1,619 @@
+/*
+ * oracle/jsvd_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU oracle for the hot path of
+ * arXiv 2202.08361 (Novakovic, "Vectorization of a thread-parallel Jacobi
+ * singular value decomposition method").  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares NO code, header, table or constant generator with the CUDA path
+ * (paper_2202_08361_b200/csrc); neither side includes the other.
+ *
+ * Every function follows the paper's algorithm statement by statement with
+ * s = 1 lanes (the scalar reading), in IEEE binary64,
+ * round-to-nearest-even, using libm fma/sqrt/logb/scalbn/fmin/fmax/copysign.
+ * Compile with -O2 -ffp-contract=off -fno-fast-math (no contraction).
+ *
+ * Citations "P:a-b" are PAPER.md line ranges; "R#k" are the readings listed in
+ * DESIGN.md section "Readings of the paper" (same numbering as SURVEY.md 8(c).4).
+ *
+ * Pins (tests/test_oracle_*.py) tie every function here to something other
+ * than itself: the paper's worked examples, closed forms, quad-precision
+ * (__float128 / mpmath) references, invariants, and brute force.
+ */
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_ENOCONV 1
+#define ORC_EINVAL (-1)
+#define ORC_ENONFINITE (-2)
+#define ORC_ERANK (-3)
+
+#define ORC_EVD_TAN 0x1u
+#define ORC_EVD_NOBACKSCALE 0x2u
+#define ORC_ZETA_ZERO INT32_MAX
+
+/* ---------------------------------------------------------------- sign-bit ops
+ * and/andnot/or/xor with -0.0.            */
+static uint64_t bits_of(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
+static double of_bits(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
+static const uint64_t SIGN = 0x8000000000000000ull;
+/* xor(x, and(y, -0)): multiplies the signs */
+static double xor_sign(double x, double y) { return of_bits(bits_of(x) ^ (bits_of(y) & SIGN)); }
+
+/* fl(sqrt(omega)) = 1.34078079299425956E+154 (R#1) */
+static const double SQRT_OMEGA = 0x1.fffffffffffffp+511;
+
+/* ---------------------------------------------------------------- Alg 2.1
+ * naive hypot: x=|x|, y=|y|, m=min, M=max, q=max(m/M,0),
+ * return sqrt(fma(q,q,1))*M.                                                 */
+double orc_hypot(double x, double y)
+{
+  x = fabs(x);
+  y = fabs(y);
+  double m = fmin(x, y), M = fmax(x, y);
+  double q = fmax(m / M, 0.0); /* max replaces 0/0 -> NaN with 0 */
+  return sqrt(fma(q, q, 1.0)) * M;
+}
+
+/* ---------------------------------------------------------------- Eq. (z)
+ * zeta = min{omega, eta - floor(lg|a_ij|) ...}, eta = 1020, lg 0 = -inf
+ * (Alg 2.2 lines 6-8).  Returned as a double exactly as
+ * in the paper (DBL_MAX for the zero matrix).                                */
+double orc_zeta(double a11, double a22, double re, double im)
+{
+  const double eta = 1020.0;
+  double z11 = eta - logb(a11), z22 = eta - logb(a22);
+  double zr = eta - logb(re), zi = eta - logb(im);
+  return fmin(DBL_MAX, fmin(fmin(z11, z22), fmin(zr, zi)));
+}
+
+/* scalef(x, zeta) with zeta = omega (the zero matrix, R#2): all entries are
+ * zero then, and any huge finite scale gives the same zeros. */
+static int zeta_int(double zd) { return zd >= 4096.0 ? 4096 : (int)zd; }
+
+/* ---------------------------------------------------------------- Alg 2.2 / SM2.1
+ * One Hermitian (is_complex) or real symmetric matrix of order two.
+ * Statement order of z8jac2 / d8jac2, s = 1.
+ * Outputs: l1, l2 (backscaled unless NOBACKSCALE), c = cos(phi),
+ * (sr, si) = e^{ia} sin(phi) (default) or e^{ia} tan(phi)
+ * under ORC_EVD_TAN; zeta (int, ORC_ZETA_ZERO for the zero matrix); p = perm. */
+void orc_evd2_one(int is_complex, double a11, double a22, double re, double im, unsigned flags,
+                  double *l1o, double *l2o, double *co, double *sro, double *sio, int32_t *zo,
+                  int *po)
+{
+  if (!is_complex) im = 0.0;
+  /* lines 6-8: the scaling exponent (Eq. z) */
+  double zd = is_complex ? orc_zeta(a11, a22, re, im) : orc_zeta(a11, a22, re, 0.0);
+  int iz = zeta_int(zd);
+  /* lines 10-11: A <- 2^zeta A */
+  re = scalbn(re, iz);
+  if (is_complex) im = scalbn(im, iz);
+  a11 = scalbn(a11, iz);
+  a22 = scalbn(a22, iz);
+  double ab, ca = 0.0, sa = 0.0;
+  if (is_complex) {
+    /* lines 12-18: polar form of a21 (Eq. zpolar) */
+    double ar = fabs(re), ai = fabs(im);
+    ab = orc_hypot(ar, ai);                         /* |a21| by Alg 2.1 */
+    ca = copysign(fmin(ar / ab, 1.0), re);          /* min replaces 0/0 with 1; or() sign */
+    sa = im / fmax(ab, DBL_TRUE_MIN);               /* max replaces 0 with mu_check */
+  } else {
+    ab = fabs(re);
+  }
+  /* lines 19-21: tan(2phi) (Eq. tan2) */
+  double o = scalbn(ab, 1);
+  double a = a11 - a22;
+  double t2 = copysign(fmin(fmax(o / fabs(a), 0.0), SQRT_OMEGA), a);
+  /* line 22-23: tan(phi) (Eq. jactan) */
+  double sec2_2 = fma(t2, t2, 1.0);
+  double t = t2 / (1.0 + sqrt(sec2_2));
+  /* lines 24-25: sec^2, sec, cos (Eq. jacsec) */
+  double s2 = fma(t, t, 1.0);
+  double se = sqrt(s2);
+  double c = 1.0 / se;
+  /* lines 26-27: e^{ia} tan(phi) */
+  double C, S;
+  if (is_complex) {
+    C = ca * t;
+    S = sa * t;
+  } else {
+    C = xor_sign(t, re); /* +-tan(phi) = xor(tan(phi), sgn(a21)) */
+    S = 0.0;
+  }
+  /* lines 28-30: eigenvalues (Eq. lamsec) */
+  double l1 = fma(t, fma(a22, t, o), a11) / s2;
+  double l2 = fma(t, fma(a11, t, -o), a22) / s2;
+  int p = (l1 < l2); /* line 32, on the scaled values */
+  if (!(flags & ORC_EVD_NOBACKSCALE)) {
+    l1 = scalbn(l1, -iz);
+    l2 = scalbn(l2, -iz);
+  }
+  double sr, si;
+  if (flags & ORC_EVD_TAN) {
+    sr = C;
+    si = S;
+  } else { /* P:793 comment: e^{ia} sin(phi) = e^{ia} tan(phi) / sec(phi) */
+    sr = C / se;
+    si = S / se;
+  }
+  *l1o = l1;
+  *l2o = l2;
+  *co = c;
+  *sro = sr;
+  if (sio) *sio = si;
+  *zo = (zd == DBL_MAX) ? ORC_ZETA_ZERO : (int32_t)iz;
+  *po = p;
+}
+
+/* Alg 2.3 zbjac2 / SM2.2 dbjac2: OpenMP over chunks
+ * of 32 matrices (one perm word each); no dependencies between iterations. */
+int orc_evd2_batched(int is_complex, int64_t r, const double *a11, const double *a22,
+                     const double *re, const double *im, double *l1, double *l2, double *c,
+                     double *sr, double *si, int32_t *zeta, uint32_t *perm, unsigned flags)
+{
+  if (r < 0 || (is_complex && (!im || !si)) || (!is_complex && (im || si))) return ORC_EINVAL;
+  int64_t nw = (r + 31) / 32;
+#pragma omp parallel for schedule(static)
+  for (int64_t w = 0; w < nw; ++w) {
+    uint32_t word = 0;
+    for (int64_t l = w * 32; l < r && l < (w + 1) * 32; ++l) {
+      int32_t z;
+      int p;
+      double dummy;
+      orc_evd2_one(is_complex, a11[l], a22[l], re[l], is_complex ? im[l] : 0.0, flags, &l1[l],
+                   &l2[l], &c[l], &sr[l], is_complex ? &si[l] : &dummy, &z, &p);
+      if (zeta) zeta[l] = z;
+      word |= (uint32_t)p << (l % 32);
+    }
+    if (perm) perm[w] = word;
+  }
+  return ORC_OK;
+}
+
+/* ================================================================== SVD step
+ * Reduction spec R (R#15): element i goes to lane floor(i/c) mod W and is
+ * accumulated in increasing i; lanes then combine as acc[L] = acc[L] + acc[L^o]
+ * for each offset o in order; the result is acc[0].                         */
+typedef struct {
+  int32_t W, c, noffs;
+  int32_t offs[32];
+} orc_rspec;
+
+static int rspec_ok(const orc_rspec *R)
+{
+  if (R->W < 1 || (R->W & (R->W - 1)) || R->c < 1 || R->noffs < 0 || R->noffs > 32) return 0;
+  int32_t cover = 0;
+  for (int k = 0; k < R->noffs; ++k) {
+    int32_t o = R->offs[k];
+    if (o <= 0 || (o & (o - 1)) || o >= R->W || (cover & o)) return 0;
+    cover |= o;
+  }
+  return cover == R->W - 1;
+}
+
+static double rspec_combine(const orc_rspec *R, double *acc)
+{
+  double *tmp = (double *)malloc(sizeof(double) * (size_t)R->W);
+  for (int k = 0; k < R->noffs; ++k) {
+    int32_t o = R->offs[k];
+    for (int32_t L = 0; L < R->W; ++L) tmp[L] = acc[L] + acc[L ^ o];
+    memcpy(acc, tmp, sizeof(double) * (size_t)R->W);
+  }
+  free(tmp);
+  return acc[0];
+}
+
+static int64_t lane_of(const orc_rspec *R, int64_t i) { return (i / R->c) % R->W; }
+
+/* element accessors: real column x[i], complex interleaved x[2i], x[2i+1] */
+static double re_at(int cplx, const double *x, int64_t i) { return cplx ? x[2 * i] : x[i]; }
+static double im_at(int cplx, const double *x, int64_t i) { return cplx ? x[2 * i + 1] : 0.0; }
+
+/* Column norm in (e,f) form (R#14):
+ *   E = logb(max over components of |x|);  y = scalbn(x, -E);
+ *   SSQ = sum over rows of fma(y_re,y_re,.) then fma(y_im,y_im,.) in spec R;
+ *   k = logb(SSQ), g = scalbn(SSQ,-k); if k odd: g = 2g, k = k-1;
+ *   f = sqrt(g), e = E + k/2.  Zero column -> (-inf, 1).                    */
+void orc_colnorm(int cplx, int64_t m, const double *x, const orc_rspec *R, double *e, double *f)
+{
+  double mx = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    mx = fmax(mx, fabs(re_at(cplx, x, i)));
+    if (cplx) mx = fmax(mx, fabs(im_at(cplx, x, i)));
+  }
+  if (mx == 0.0) {
+    *e = -INFINITY;
+    *f = 1.0;
+    return;
+  }
+  int E = (int)logb(mx);
+  double *acc = (double *)calloc((size_t)R->W, sizeof(double));
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t L = lane_of(R, i);
+    double yr = scalbn(re_at(cplx, x, i), -E);
+    acc[L] = fma(yr, yr, acc[L]);
+    if (cplx) {
+      double yi = scalbn(im_at(cplx, x, i), -E);
+      acc[L] = fma(yi, yi, acc[L]);
+    }
+  }
+  double ssq = rspec_combine(R, acc);
+  free(acc);
+  int k = (int)logb(ssq);
+  double g = scalbn(ssq, -k);
+  if (k & 1) { /* odd exponent: f' = 2f, e' = e - 1 */
+    g = 2.0 * g;
+    k = k - 1;
+  }
+  *f = sqrt(g);
+  *e = (double)(E + k / 2);
+}
+
+/* Alg 3.1 zdpscl: columns prescaled by 2^{-e_j}, fma schedule
+ * of lines 5-6 (re += Rq*Rp + Iq*Ip; im += Rq*Ip - Iq*Rp), reduction in spec R,
+ * one division of both components by fl(f_q * f_p).  Real: its simplification.
+ * A zero column (e = -inf) gives z = 0 (R#19).                               */
+void orc_dot(int cplx, int64_t m, const double *xq, double eq, double fq, const double *xp,
+             double ep, double fp, const orc_rspec *R, double *zre, double *zim)
+{
+  if (isinf(eq) || isinf(ep)) {
+    *zre = 0.0;
+    *zim = 0.0;
+    return;
+  }
+  int iq = (int)eq, ip = (int)ep;
+  double *ar = (double *)calloc((size_t)R->W, sizeof(double));
+  double *ai = (double *)calloc((size_t)R->W, sizeof(double));
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t L = lane_of(R, i);
+    double rq = scalbn(re_at(cplx, xq, i), -iq), rp = scalbn(re_at(cplx, xp, i), -ip);
+    if (cplx) {
+      double jq = scalbn(im_at(cplx, xq, i), -iq), jp = scalbn(im_at(cplx, xp, i), -ip);
+      ar[L] = fma(rq, rp, ar[L]);  /* line 5 */
+      ai[L] = fma(rq, jp, ai[L]);
+      ar[L] = fma(jq, jp, ar[L]);  /* line 6 */
+      ai[L] = fma(-jq, rp, ai[L]); /* fnmadd */
+    } else {
+      ar[L] = fma(rq, rp, ar[L]);
+    }
+  }
+  double zr = rspec_combine(R, ar);
+  double zi = cplx ? rspec_combine(R, ai) : 0.0;
+  free(ar);
+  free(ai);
+  double d = fq * fp; /* line 8: single division by fl(f_q f_p) */
+  *zre = zr / d;
+  *zim = cplx ? zi / d : 0.0;
+}
+
+/* Alg 3.2: transform iff upsilon <= fl(|z|) (naive hypot). */
+int orc_cvg(double zre, double zim, double upsilon) { return upsilon <= orc_hypot(zre, zim); }
+
+/* upsilon = fl(eps * sqrt(m)), eps = 2^-53 (Eq. tol; R#18) */
+double orc_upsilon(int64_t m) { return scalbn(sqrt((double)m), -53); }
+
+/* getmant(x, NORM_1_2, SIGN_zero) (Eq. F) */
+static double getmant12(double x) { return scalbn(fabs(x), -(int)logb(x)); }
+
+/* Alg 3.3: non-overflowing scaled Grammian of the pair. */
+void orc_gram(double zre, double zim, double e1, double f1, double e2, double f2, double *a11,
+              double *a22, double *b21re, double *b21im)
+{
+  double f12 = f1 / f2, e12 = e1 - e2; /* line 1 */
+  double f21 = f2 / f1, e21 = e2 - e1;
+  e12 = e12 + logb(f12); /* line 2 */
+  f12 = getmant12(f12);
+  e21 = e21 + logb(f21); /* line 3 */
+  f21 = getmant12(f21);
+  double sA = fmin(1023.0 - fmax(e12, e21), 0.0); /* line 4: eta_hat = DBL_MAX_EXP-1 */
+  e12 = e12 + sA;                                 /* line 5 */
+  e21 = e21 + sA;
+  *a11 = scalbn(f12, (int)e12); /* line 6 */
+  *a22 = scalbn(f21, (int)e21);
+  *b21re = scalbn(zre, (int)sA); /* line 7 */
+  *b21im = scalbn(zim, (int)sA);
+}
+
+/* Alg 3.4 zjrot / djrot with P = I (R#20): the fma schedule of
+ * lines 5-6 and 9-10 (Eq. zfma + Eq. transf).  Returns max |component| of the
+ * transformed columns.                                                       */
+double orc_rot(int cplx, int64_t l, double *xp, double *xq, double c, double C, double S)
+{
+  double M = 0.0;
+  for (int64_t i = 0; i < l; ++i) {
+    if (cplx) {
+      double rp = xp[2 * i], ip = xp[2 * i + 1], rq = xq[2 * i], iq = xq[2 * i + 1];
+      double rp2 = fma(rq, C, fma(-iq, S, rp)) * c; /* line 5 */
+      double ip2 = fma(rq, S, fma(iq, C, ip)) * c;  /* line 6 */
+      double rq2 = fma(rp, -C, fma(-ip, S, rq)) * c; /* line 9 */
+      double iq2 = fma(rp, S, fma(ip, -C, iq)) * c;  /* line 10 */
+      xp[2 * i] = rp2;
+      xp[2 * i + 1] = ip2;
+      xq[2 * i] = rq2;
+      xq[2 * i + 1] = iq2;
+      M = fmax(M, fmax(fabs(rp2), fabs(ip2)));
+      M = fmax(M, fmax(fabs(rq2), fabs(iq2)));
+    } else {
+      double p = xp[i], q = xq[i];
+      double p2 = fma(q, C, p) * c;
+      double q2 = fma(p, -C, q) * c;
+      xp[i] = p2;
+      xq[i] = q2;
+      M = fmax(M, fmax(fabs(p2), fabs(q2)));
+    }
+  }
+  return M;
+}
+
+/* One step of Alg 4.1 lines 7-38 over explicit disjoint pairs,
+ * s = 1 (R#13), P = I (R#20).  col_e/col_f receive the norms of the step's
+ * columns BEFORE rotation; *t += transformed pairs; *mmax = max(*mmax, M).   */
+int orc_step(int cplx, int64_t m, int64_t n, double *G, int64_t ldg, double *V, int64_t ldv,
+             const int32_t *pairs, int64_t npairs, double tol, const orc_rspec *R,
+             double *col_e, double *col_f, int64_t *t_out, double *mmax)
+{
+  if (!rspec_ok(R) || m < 1 || n < 2 || ldg < m || (V && ldv < n)) return ORC_EINVAL;
+  const int64_t w = cplx ? 2 : 1;
+  double upsilon = tol > 0.0 ? tol : orc_upsilon(m);
+  int64_t t = 0;
+  double M = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : t) reduction(max : M)
+  for (int64_t l = 0; l < npairs; ++l) {
+    int64_t p = pairs[2 * l], q = pairs[2 * l + 1];
+    double *gp = G + w * p * ldg, *gq = G + w * q * ldg;
+    double ep, fp, eq, fq;
+    orc_colnorm(cplx, m, gp, R, &ep, &fp); /* spade: norms */
+    orc_colnorm(cplx, m, gq, R, &eq, &fq);
+    col_e[p] = ep;
+    col_f[p] = fp;
+    col_e[q] = eq;
+    col_f[q] = fq;
+    double zr, zi;
+    orc_dot(cplx, m, gq, eq, fq, gp, ep, fp, R, &zr, &zi); /* club: a21' = gq^* gp */
+    if (!orc_cvg(zr, zi, upsilon)) continue;                /* heart: Alg 3.2 */
+    double b11, b22, br, bi;
+    orc_gram(zr, zi, ep, fp, eq, fq, &b11, &b22, &br, &bi); /* heart: Alg 3.3 */
+    double l1, l2, c, C, S;
+    int32_t z;
+    int pp;
+    orc_evd2_one(cplx, b11, b22, br, bi, ORC_EVD_TAN | ORC_EVD_NOBACKSCALE, &l1, &l2, &c, &C, &S,
+                 &z, &pp); /* diamond */
+    double Mp = orc_rot(cplx, m, gp, gq, c, C, S); /* star: G */
+    if (V) orc_rot(cplx, n, V + w * p * ldv, V + w * q * ldv, c, C, S); /* star: V */
+    if (Mp > M) M = Mp;
+    t += 1;
+  }
+  *t_out += t;
+  if (M > *mmax) *mmax = M;
+  return ORC_OK;
+}
+
+/* ================================================================ strategy
+ * R#20.  Flat round-robin (circle method) on P players, round r in [0,P-1):
+ * position 0 = player 0, position k>=1 = player ((k-1+r) mod (P-1)) + 1;
+ * pairs are positions (i, P-1-i), i in [0, P/2).                            */
+static void circle(int64_t P, int64_t r, int64_t i, int64_t *a, int64_t *b)
+{
+  int64_t pos[2] = {i, P - 1 - i}, pl[2];
+  for (int k = 0; k < 2; ++k) pl[k] = pos[k] == 0 ? 0 : ((pos[k] - 1 + r) % (P - 1)) + 1;
+  *a = pl[0] < pl[1] ? pl[0] : pl[1];
+  *b = pl[0] < pl[1] ? pl[1] : pl[0];
+}
+
+/* Block round-robin with B blocks of b = n/B columns (b even or b == 1):
+ *  phase I  (steps 0..b-2): flat RR inside every block;
+ *  phase II (B-1 rounds of b steps): rounds of flat RR over blocks; in round
+ *  rr, block pair (beta, beta') runs b steps, step tt pairing column j of beta
+ *  with column (j+tt) mod b of beta'.  n-1 steps, n/2 disjoint pairs each.
+ *  Pairs listed block-pair by block-pair; (p, q) with p < q.                */
+int orc_strategy_pairs(int64_t n, int64_t B, int64_t step, int32_t *pairs)
+{
+  if (n < 2 || (n & 1) || B < 2 || n % B) return ORC_EINVAL;
+  int64_t b = n / B;
+  if (b > 1 && (b & 1)) return ORC_EINVAL;
+  if (step < 0 || step >= n - 1) return ORC_EINVAL;
+  int64_t l = 0;
+  if (step < b - 1) {
+    for (int64_t beta = 0; beta < B; ++beta)
+      for (int64_t i = 0; i < b / 2; ++i) {
+        int64_t x, y;
+        circle(b, step, i, &x, &y);
+        pairs[2 * l] = (int32_t)(beta * b + x);
+        pairs[2 * l + 1] = (int32_t)(beta * b + y);
+        ++l;
+      }
+    return ORC_OK;
+  }
+  int64_t s2 = step - (b - 1);
+  int64_t rr = s2 / b, tt = s2 % b;
+  for (int64_t i = 0; i < B / 2; ++i) {
+    int64_t be, bf;
+    circle(B, rr, i, &be, &bf);
+    for (int64_t j = 0; j < b; ++j) {
+      int64_t x = be * b + j, y = bf * b + (j + tt) % b;
+      pairs[2 * l] = (int32_t)(x < y ? x : y);
+      pairs[2 * l + 1] = (int32_t)(x < y ? y : x);
+      ++l;
+    }
+  }
+  return ORC_OK;
+}
+
+/* rescale check points (R#21): start of phase I and of every phase-II round */
+int orc_strategy_is_checkpoint(int64_t n, int64_t B, int64_t step)
+{
+  int64_t b = n / B;
+  if (step == 0) return 1;
+  if (step < b - 1) return 0;
+  return ((step - (b - 1)) % b) == 0;
+}
+
+/* ================================================================ driver
+ * Alg 4.1 zvjsvd / dvjsvd with s = 1, P = I, the scaled norms
+ * of R#14, the rescaling heuristic of P:1071-1115 (Eqs. skn/skr, exact integer
+ * floors R#28), finalize of P:1473-1485 and the sort of R#24.               */
+
+/* floor(lg(omega / (varsigma m))) (real) / floor(lg(omega/(varsigma m sqrt2))) (complex) */
+int orc_Fm(int cplx, int64_t m)
+{
+  int k = 0;
+  while ((m >> (k + 1)) > 0) ++k; /* k = floor(lg m) */
+  if (!cplx) return 1022 - k;
+  /* m^2 >= 2^(2k+1)  <=>  lg m >= k + 1/2 */
+  unsigned __int128 mm = (unsigned __int128)m * (unsigned __int128)m;
+  unsigned __int128 th = (unsigned __int128)1 << (2 * k + 1);
+  return 1021 - k - (mm >= th ? 1 : 0);
+}
+
+/* M-tilde: max over components of |entry|, NaN -> inf */
+static double maxnorm(int cplx, int64_t m, int64_t n, const double *G, int64_t ldg)
+{
+  double x = 0.0;
+  int64_t w = cplx ? 2 : 1;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < w * m; ++i) x = fmax(x, fmin(fabs(G[w * j * ldg + i]), INFINITY));
+  return x;
+}
+
+static void scale_matrix(int cplx, int64_t m, int64_t n, double *G, int64_t ldg, int s)
+{
+  int64_t w = cplx ? 2 : 1;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < w * m; ++i) G[w * j * ldg + i] = scalbn(G[w * j * ldg + i], s);
+}
+
+int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V, int64_t ldv,
+              double *sigma, double *sigma_e, double *sigma_f, int64_t B, int32_t max_sweeps,
+              int32_t *sweeps_done, int64_t *tps, const orc_rspec *R)
+{
+  if (m < n || n < 2 || (n & 1) || lda < m || ldv < n || !rspec_ok(R) || max_sweeps < 0)
+    return ORC_EINVAL;
+  if (B != n && (n % B || ((n / B) & 1))) return ORC_EINVAL;
+  const int64_t w = cplx ? 2 : 1;
+  /* line 1: M0, s0, G1 = 2^s0 G0 (Eq. skn) */
+  double Mt = maxnorm(cplx, m, n, A, lda);
+  if (isinf(Mt)) return ORC_ENONFINITE;
+  if (Mt == 0.0) return ORC_ERANK;
+  const int Fm = orc_Fm(cplx, m);
+  const int Kr = cplx ? 1020 : 1022; /* floor(lg(omega/varsigma)) [-1]: Eq. skr */
+  int s = Fm - (int)logb(Mt) - 1;
+  scale_matrix(cplx, m, n, A, lda, s);
+  Mt = scalbn(Mt, s);
+  /* line 2: V = I */
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < w * n; ++i) V[w * j * ldv + i] = (i == w * j) ? 1.0 : 0.0;
+  double *ce = (double *)malloc(sizeof(double) * (size_t)n);
+  double *cf = (double *)malloc(sizeof(double) * (size_t)n);
+  int32_t *pairs = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+  double upsilon = orc_upsilon(m);
+  int32_t C = 0;
+  int converged = 0;
+  for (C = 0; C < max_sweeps; ++C) { /* line 3 */
+    int64_t T = 0;
+    for (int64_t k = 0; k < n - 1; ++k) { /* line 5 */
+      if (orc_strategy_is_checkpoint(n, B, k)) { /* line 6 (R#21) */
+        int sk = Kr - (int)logb(Mt);
+        if (sk < 0) {
+          int sn = Fm - (int)logb(Mt) - 1;
+          scale_matrix(cplx, m, n, A, lda, sn);
+          Mt = scalbn(Mt, sn);
+          s += sn;
+        }
+      }
+      orc_strategy_pairs(n, B, k, pairs);
+      int64_t t = 0;
+      double M = 0.0;
+      orc_step(cplx, m, n, A, lda, V, ldv, pairs, n / 2, upsilon, R, ce, cf, &t, &M);
+      T += t;
+      Mt = fmax(Mt, M); /* line 38 */
+    }
+    if (tps) tps[C] = T;
+    if (T == 0) { /* line 40 */
+      converged = 1;
+      ++C;
+      break;
+    }
+  }
+  if (sweeps_done) *sweeps_done = C;
+  /* finalize: norms of the final columns.  If converged they
+   * equal those of the last sweep; recomputing them with the same R is
+   * bit-identical and also defines the result for a capped run (R#25).     */
+  for (int64_t j = 0; j < n; ++j) orc_colnorm(cplx, m, A + w * j * lda, R, &ce[j], &cf[j]);
+  for (int64_t j = 0; j < n; ++j) {
+    double *g = A + w * j * lda;
+    if (!isinf(ce[j])) {
+      int ej = (int)ce[j];
+      for (int64_t i = 0; i < w * m; ++i) g[i] = scalbn(g[i], -ej) / cf[j];
+      ce[j] = ce[j] - s;
+    }
+  }
+  /* sort sigma non-increasing (R#24): by (e, f) descending, ties by index */
+  int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t j = 0; j < n; ++j) perm[j] = j;
+  for (int64_t i = 1; i < n; ++i) { /* stable insertion sort */
+    int64_t pj = perm[i], k = i - 1;
+    while (k >= 0) {
+      int64_t pk = perm[k];
+      int greater = (ce[pj] > ce[pk]) || (ce[pj] == ce[pk] && cf[pj] > cf[pk]);
+      if (!greater) break;
+      perm[k + 1] = pk;
+      --k;
+    }
+    perm[k + 1] = pj;
+  }
+  double *tmpA = (double *)malloc(sizeof(double) * (size_t)(w * m * n));
+  double *tmpV = (double *)malloc(sizeof(double) * (size_t)(w * n * n));
+  for (int64_t j = 0; j < n; ++j) {
+    memcpy(tmpA + w * j * m, A + w * perm[j] * lda, sizeof(double) * (size_t)(w * m));
+    memcpy(tmpV + w * j * n, V + w * perm[j] * ldv, sizeof(double) * (size_t)(w * n));
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    memcpy(A + w * j * lda, tmpA + w * j * m, sizeof(double) * (size_t)(w * m));
+    memcpy(V + w * j * ldv, tmpV + w * j * n, sizeof(double) * (size_t)(w * n));
+    double e = ce[perm[j]], f = cf[perm[j]];
+    if (sigma_e) sigma_e[j] = e;
+    if (sigma_f) sigma_f[j] = f;
+    if (sigma) sigma[j] = isinf(e) ? 0.0 : scalbn(f, (int)fmax(fmin(e, 1e5), -1e5));
+  }
+  free(tmpA);
+  free(tmpV);
+  free(perm);
+  free(ce);
+  free(cf);
+  free(pairs);
+  return converged ? ORC_OK : ORC_ENOCONV;
+}
+
+/* A batch of independent SVDs (configuration 4); OpenMP over matrices. */
+int orc_gesvj_batched(int cplx, int64_t batch, int64_t m, int64_t n, double *A, int64_t lda,
+                      int64_t strideA, double *V, int64_t ldv, int64_t strideV, double *sigma,
+                      int32_t max_sweeps, int32_t *sweeps_done, int32_t *status,
+                      const orc_rspec *R)
+{
+  const int64_t w = cplx ? 2 : 1;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < batch; ++b) {
+    int32_t sw = 0;
+    int st = orc_gesvj(cplx, m, n, A + w * b * strideA, lda, V + w * b * strideV, ldv,
+                       sigma + b * n, NULL, NULL, n, max_sweeps, &sw, NULL, R);
+    if (sweeps_done) sweeps_done[b] = sw;
+    if (status) status[b] = st;
+  }
+  return ORC_OK;
+}
+
+int orc_num_threads(void)
+{
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
