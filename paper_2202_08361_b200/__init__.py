@@ -1,0 +1,238 @@
+"""paper_2202_08361_b200 -- B200-native hot path of arXiv 2202.08361.
+
+Thin Python binding over the C ABI of ``libjsvd.so`` (``include/jsvd.h``): the
+functions here only marshal torch CUDA tensors into pointers, sizes and the
+current CUDA stream; every step of the method runs in the library's sm_100a
+kernels.  There is no CPU fallback: if the library is missing or no CUDA
+device is present, the calls raise.
+
+Entry points (same names as the C ABI, minus the ``jsvd_`` prefix):
+  evd2_batched  -- Alg 2.2/2.3, SM2.1/SM2.2 batched 2x2 EVD
+  sweep_step    -- one parallel Jacobi step, Alg 4.1 lines 7-38
+  gesvj         -- the full one-sided Jacobi SVD, Alg 4.1
+  gesvj_batched -- a batch of small independent SVDs (BASELINE configs[3])
+"""
+import ctypes as ct
+import os
+
+import torch
+
+from ._build import LIB
+
+__all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "strategy_pairs", "gesvj",
+           "gesvj_workspace", "gesvj_batched", "launch_count", "JsvdError", "R64", "C64",
+           "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
+
+R64, C64 = 0, 1
+EVD_TAN, EVD_NOBACKSCALE = 0x1, 0x2
+ZETA_ZERO = 2 ** 31 - 1
+OK, ENOCONV = 0, 1
+
+
+class JsvdError(RuntimeError):
+    def __init__(self, status, where):
+        super().__init__(f"{where}: {status_string(status)} ({status})")
+        self.status = status
+
+
+_lib = None
+_vp, _i64, _i32, _d = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_double
+
+
+def lib():
+    """Load libjsvd.so (built by __graft_entry__.build()); raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"{LIB} is missing: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = ct.CDLL(LIB)
+        L.jsvd_evd2_batched.restype = ct.c_int
+        L.jsvd_evd2_batched.argtypes = [ct.c_int, _i64] + [_vp] * 11 + [ct.c_uint32, _vp]
+        L.jsvd_sweep_step.restype = ct.c_int
+        L.jsvd_sweep_step.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _d,
+                                      _vp, _vp, _vp, _vp, _vp]
+        L.jsvd_step_rspec.restype = ct.c_int
+        L.jsvd_step_rspec.argtypes = [ct.c_int, _i64] + [ct.POINTER(_i32)] * 2 + [_vp,
+                                                                                   ct.POINTER(_i32)]
+        L.jsvd_strategy_pairs.restype = ct.c_int
+        L.jsvd_strategy_pairs.argtypes = [_i64, _i32, _i64, _vp, _vp]
+        L.jsvd_gesvj_workspace.restype = ct.c_int
+        L.jsvd_gesvj_workspace.argtypes = [ct.c_int, _i64, _i64, ct.POINTER(ct.c_size_t)]
+        L.jsvd_gesvj.restype = ct.c_int
+        L.jsvd_gesvj.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i32,
+                                 _i32, ct.POINTER(_i32), _vp, _vp, ct.c_size_t, _vp]
+        L.jsvd_gesvj_batched.restype = ct.c_int
+        L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
+                                         _i64, _vp, _i32, _vp, _vp, _vp]
+        L.jsvd_status_string.restype = ct.c_char_p
+        L.jsvd_status_string.argtypes = [ct.c_int]
+        L.jsvd_launch_count.restype = _i64
+        L.jsvd_launch_count.argtypes = []
+        _lib = L
+    return _lib
+
+
+def status_string(s):
+    return lib().jsvd_status_string(int(s)).decode()
+
+
+def launch_count():
+    return int(lib().jsvd_launch_count())
+
+
+def _check(st, where, allow=(OK,)):
+    if st not in allow:
+        raise JsvdError(st, where)
+    return st
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ct.c_void_p(stream.cuda_stream)
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("jsvd expects CUDA tensors (no CPU fallback)")
+    return ct.c_void_p(t.data_ptr())
+
+
+def _f64(t, name):
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+    return t
+
+
+def evd2_batched(a11, a22, a21_re, a21_im=None, flags=0, out=None, stream=None):
+    """Batched EVD of 2x2 Hermitian (a21_im given) / symmetric matrices.
+
+    a11, a22, a21_re, a21_im: float64 CUDA tensors of length r (SoA).
+    Returns dict(lam1, lam2, cos, sin_re[, sin_im], zeta, perm); pass ``out`` (a
+    dict of preallocated tensors with those keys) to avoid allocation.
+    """
+    cplx = a21_im is not None
+    r = a11.numel()
+    for n_, t in (("a11", a11), ("a22", a22), ("a21_re", a21_re)) + ((("a21_im", a21_im),) if cplx else ()):
+        _f64(t, n_)
+        if t.numel() != r:
+            raise ValueError("all input streams must have the same length")
+    if out is None:
+        dev = a11.device
+        out = {k: torch.empty(r, dtype=torch.float64, device=dev) for k in ("lam1", "lam2", "cos", "sin_re")}
+        out["sin_im"] = torch.empty(r, dtype=torch.float64, device=dev) if cplx else None
+        out["zeta"] = torch.empty(r, dtype=torch.int32, device=dev)
+        out["perm"] = torch.empty((r + 31) // 32, dtype=torch.int32, device=dev)
+    st = lib().jsvd_evd2_batched(
+        C64 if cplx else R64, r, _p(a11), _p(a22), _p(a21_re), _p(a21_im), _p(out["lam1"]),
+        _p(out["lam2"]), _p(out["cos"]), _p(out["sin_re"]), _p(out.get("sin_im")),
+        _p(out.get("zeta")), _p(out.get("perm")), flags, _stream(stream))
+    _check(st, "jsvd_evd2_batched")
+    return out
+
+
+def step_rspec(cplx, m):
+    """(W, c, offsets) of the step kernel the library picks for (dtype, m)."""
+    W, c, no = _i32(), _i32(), _i32()
+    offs = (_i32 * 32)()
+    _check(lib().jsvd_step_rspec(C64 if cplx else R64, m, ct.byref(W), ct.byref(c),
+                                 ct.cast(offs, _vp), ct.byref(no)), "jsvd_step_rspec")
+    return W.value, c.value, tuple(offs[k] for k in range(no.value))
+
+
+def strategy_pairs(n, nblocks, step, out=None, stream=None, device="cuda"):
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=device)
+    _check(lib().jsvd_strategy_pairs(n, nblocks, step, _p(out), _stream(stream)),
+           "jsvd_strategy_pairs")
+    return out.view(-1, 2)
+
+
+def _mat(t, name):
+    """column-major (m, n) CUDA tensor (float64 or complex128) -> (cplx, ld)."""
+    if t.dtype not in (torch.float64, torch.complex128):
+        raise ValueError(f"{name} must be float64 or complex128")
+    m, n = t.shape
+    if t.stride(0) != 1 or (n > 1 and t.stride(1) < m):
+        raise ValueError(f"{name} must be column-major (use A.T.contiguous().T)")
+    return t.dtype == torch.complex128, max(t.stride(1), m) if n > 1 else m
+
+
+def sweep_step(G, V, pairs, tol=0.0, col_e=None, col_f=None, t_dev=None, mmax_dev=None,
+               stream=None):
+    """One Jacobi step in place on column-major G (m x n) and V (n x n)."""
+    cplx, ldg = _mat(G, "G")
+    m, n = G.shape
+    ldv = n
+    if V is not None:
+        cv, ldv = _mat(V, "V")
+        if cv != cplx or V.shape != (n, n):
+            raise ValueError("V must be n x n of G's dtype")
+    dev = G.device
+    col_e = torch.empty(n, dtype=torch.float64, device=dev) if col_e is None else col_e
+    col_f = torch.empty(n, dtype=torch.float64, device=dev) if col_f is None else col_f
+    t_dev = torch.zeros(1, dtype=torch.int64, device=dev) if t_dev is None else t_dev
+    mmax_dev = torch.zeros(1, dtype=torch.float64, device=dev) if mmax_dev is None else mmax_dev
+    pairs = pairs.reshape(-1)
+    if pairs.dtype != torch.int32 or not pairs.is_contiguous():
+        raise ValueError("pairs must be contiguous int32")
+    st = lib().jsvd_sweep_step(C64 if cplx else R64, m, n, _p(G), ldg, _p(V), ldv, _p(pairs),
+                               pairs.numel() // 2, float(tol), _p(col_e), _p(col_f), _p(t_dev),
+                               _p(mmax_dev), _stream(stream))
+    _check(st, "jsvd_sweep_step")
+    return dict(col_e=col_e, col_f=col_f, t=t_dev, mmax=mmax_dev)
+
+
+def gesvj_workspace(cplx, m, n):
+    b = ct.c_size_t()
+    _check(lib().jsvd_gesvj_workspace(C64 if cplx else R64, m, n, ct.byref(b)),
+           "jsvd_gesvj_workspace")
+    return b.value
+
+
+def gesvj(A, nblocks=None, max_sweeps=30, V=None, work=None, stream=None):
+    """Full SVD in place: A (column-major m x n) becomes U.  Returns dict."""
+    cplx, lda = _mat(A, "A")
+    m, n = A.shape
+    dev = A.device
+    if V is None:
+        V = torch.empty((n, n), dtype=A.dtype, device=dev).T.contiguous().T
+    _, ldv = _mat(V, "V")
+    sig = torch.empty(n, dtype=torch.float64, device=dev)
+    se = torch.empty(n, dtype=torch.float64, device=dev)
+    sf = torch.empty(n, dtype=torch.float64, device=dev)
+    wb = gesvj_workspace(cplx, m, n)
+    if work is None or work.numel() < wb:
+        work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    sw = _i32(0)
+    tps = (_i64 * max(max_sweeps, 1))()
+    st = lib().jsvd_gesvj(C64 if cplx else R64, m, n, _p(A), lda, _p(V), ldv, _p(sig), _p(se),
+                          _p(sf), n if nblocks is None else nblocks, max_sweeps, ct.byref(sw),
+                          ct.cast(tps, _vp), _p(work), work.numel(), _stream(stream))
+    _check(st, "jsvd_gesvj", allow=(OK, ENOCONV))
+    return dict(U=A, V=V, sigma=sig, sigma_e=se, sigma_f=sf, sweeps=sw.value,
+                tps=[tps[k] for k in range(sw.value)], status=st)
+
+
+def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None, stream=None):
+    """A: (batch, m, n) CUDA tensor whose matrices are column-major, i.e.
+    A.stride() == (m*n, 1, m) (use X.transpose(1,2).contiguous().transpose(1,2)).
+    In place: A becomes U.  Returns dict(U, V, sigma, sweeps, status)."""
+    b, m, n = A.shape
+    if A.dtype not in (torch.float64, torch.complex128) or A.stride(1) != 1 or A.stride(2) < m:
+        raise ValueError("A must be float64/complex128 with column-major matrices")
+    cplx = A.dtype == torch.complex128
+    dev = A.device
+    if V is None:
+        V = torch.empty((b, n, n), dtype=A.dtype, device=dev).transpose(1, 2)
+    sigma = torch.empty((b, n), dtype=torch.float64, device=dev) if sigma is None else sigma
+    sweeps = torch.empty(b, dtype=torch.int32, device=dev) if sweeps is None else sweeps
+    status = torch.empty(b, dtype=torch.int32, device=dev) if status is None else status
+    st = lib().jsvd_gesvj_batched(C64 if cplx else R64, b, m, n, _p(A), A.stride(2), A.stride(0),
+                                  _p(V), V.stride(2), V.stride(0), _p(sigma), max_sweeps,
+                                  _p(sweeps), _p(status), _stream(stream))
+    _check(st, "jsvd_gesvj_batched")
+    return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status)

@@ -1,0 +1,165 @@
+// evd2.cu -- jsvd_evd2_batched: the batched 2x2 Hermitian / symmetric EVD
+// (Alg 2.2/2.3, SM2.1/SM2.2) on sm_100a.
+//
+// HBM-streaming kernel: each thread owns K = 2 consecutive matrices, loads
+// every SoA input stream with one 16-byte LDG.128 (coalesced, 512 B per warp
+// per stream), runs the EVD in registers, and stores every output stream with
+// one 16-byte STG.128; the permutation words are assembled from two
+// warp ballots.  No shared memory, no synchronisation.  Grid: one 256-thread
+// CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110 waves at 8 CTAs/SM).
+#include "jsvd_dev.cuh"
+#include "jsvd_host.h"
+
+namespace jsvd {
+
+// spread the low 16 bits of x to the even bit positions
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+template <bool CPLX, bool TAN, bool NOBACK>
+__global__ void __launch_bounds__(256) evd2_vec2_kernel(
+    int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
+    const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
+    double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t l0 = 2 * tid;
+  bool p0 = false, p1 = false;
+  if (l0 + 1 < r) {
+    const double2 x11 = __ldcs(reinterpret_cast<const double2*>(a11) + tid);
+    const double2 x22 = __ldcs(reinterpret_cast<const double2*>(a22) + tid);
+    const double2 xre = __ldcs(reinterpret_cast<const double2*>(are) + tid);
+    double2 xim = make_double2(0.0, 0.0);
+    if (CPLX) xim = __ldcs(reinterpret_cast<const double2*>(aim) + tid);
+    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x11.x, x22.x, xre.x, xim.x);
+    const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x11.y, x22.y, xre.y, xim.y);
+    __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
+    __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
+    __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
+    __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
+    if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
+    if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
+    p0 = e0.perm;
+    p1 = e1.perm;
+  } else if (l0 < r) {  // ragged tail: one matrix
+    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(a11[l0], a22[l0], are[l0], CPLX ? aim[l0] : 0.0);
+    l1[l0] = e0.l1;
+    l2[l0] = e0.l2;
+    cs[l0] = e0.c;
+    sr[l0] = e0.sr;
+    if (CPLX) si[l0] = e0.si;
+    if (zeta) zeta[l0] = e0.zeta;
+    p0 = e0.perm;
+  }
+  if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
+    const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
+    const int64_t nwords = (r + 31) / 32;
+    if (lane < 2 && wbase + lane < nwords) {
+      const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
+      perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
+    }
+  }
+}
+
+// scalar path for pointers that are only 8-byte aligned
+template <bool CPLX, bool TAN, bool NOBACK>
+__global__ void __launch_bounds__(256) evd2_scalar_kernel(
+    int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
+    const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
+    double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool p = false;
+  if (l < r) {
+    const Evd2Out e = evd2<CPLX, TAN, NOBACK>(a11[l], a22[l], are[l], CPLX ? aim[l] : 0.0);
+    l1[l] = e.l1;
+    l2[l] = e.l2;
+    cs[l] = e.c;
+    sr[l] = e.sr;
+    if (CPLX) si[l] = e.si;
+    if (zeta) zeta[l] = e.zeta;
+    p = e.perm;
+  }
+  if (perm) {
+    const uint32_t b = __ballot_sync(0xffffffffu, p);
+    if ((threadIdx.x & 31) == 0 && l < r) perm[l / 32] = b;
+  }
+}
+
+template <bool CPLX, bool TAN, bool NOBACK>
+static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const double* a22,
+                               const double* re, const double* im, double* l1, double* l2,
+                               double* c, double* sr, double* si, int32_t* zeta, uint32_t* perm,
+                               cudaStream_t st) {
+  const int threads = 256;
+  if (vec) {
+    const int64_t blocks = (r + 2 * threads - 1) / (2 * threads);
+    evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+  } else {
+    const int64_t blocks = (r + threads - 1) / threads;
+    evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <bool CPLX>
+static cudaError_t dispatch_flags(uint32_t flags, bool vec, int64_t r, const double* a11,
+                                  const double* a22, const double* re, const double* im,
+                                  double* l1, double* l2, double* c, double* sr, double* si,
+                                  int32_t* zeta, uint32_t* perm, cudaStream_t st) {
+  const bool tan = flags & JSVD_EVD_TAN, nob = flags & JSVD_EVD_NOBACKSCALE;
+  if (tan && nob)
+    return launch_evd2<CPLX, true, true>(vec, r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm, st);
+  if (tan)
+    return launch_evd2<CPLX, true, false>(vec, r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm, st);
+  if (nob)
+    return launch_evd2<CPLX, false, true>(vec, r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm, st);
+  return launch_evd2<CPLX, false, false>(vec, r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm, st);
+}
+
+}  // namespace jsvd
+
+static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+extern "C" jsvd_status jsvd_evd2_batched(jsvd_dtype dt, int64_t r, const double* a11,
+                                         const double* a22, const double* a21_re,
+                                         const double* a21_im, double* lam1, double* lam2,
+                                         double* cos_phi, double* sin_re, double* sin_im,
+                                         int32_t* zeta, uint32_t* perm, uint32_t flags,
+                                         void* stream) {
+  using namespace jsvd;
+  if (r < 0 || (dt != JSVD_R64 && dt != JSVD_C64)) return JSVD_EINVAL;
+  if (flags & ~(JSVD_EVD_TAN | JSVD_EVD_NOBACKSCALE)) return JSVD_EINVAL;
+  if (r == 0) return JSVD_OK;
+  if (r > (int64_t(1) << 40)) return JSVD_EINVAL;
+  const bool cplx = (dt == JSVD_C64);
+  if (!a11 || !a22 || !a21_re || !lam1 || !lam2 || !cos_phi || !sin_re) return JSVD_EINVAL;
+  if (cplx != (a21_im != nullptr) || cplx != (sin_im != nullptr)) return JSVD_EINVAL;
+  const void* ptrs[] = {a11, a22, a21_re, a21_im, lam1, lam2, cos_phi, sin_re, sin_im};
+  bool vec = true;
+  for (const void* p : ptrs) {
+    if (p && !aligned(p, 8)) return JSVD_EINVAL;
+    if (p && !aligned(p, 16)) vec = false;
+  }
+  if (zeta && !aligned(zeta, 4)) return JSVD_EINVAL;
+  if (zeta && !aligned(zeta, 8)) vec = false;
+  if (perm && !aligned(perm, 4)) return JSVD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cplx ? dispatch_flags<true>(flags, vec, r, a11, a22, a21_re, a21_im, lam1, lam2,
+                                              cos_phi, sin_re, sin_im, zeta, perm, st)
+                       : dispatch_flags<false>(flags, vec, r, a11, a22, a21_re, nullptr, lam1,
+                                               lam2, cos_phi, sin_re, nullptr, zeta, perm, st);
+  return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
+}
