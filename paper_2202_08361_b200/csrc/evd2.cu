@@ -163,3 +163,21 @@ extern "C" jsvd_status jsvd_evd2_batched(jsvd_dtype dt, int64_t r, const double*
                                                lam2, cos_phi, sin_re, nullptr, zeta, perm, st);
   return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
 }
+
+// diagnostic entry point: q[i] = a[i] / b[i] with the library's division
+namespace jsvd {
+__global__ void debug_div_kernel(int64_t n, const double* a, const double* b, double* q, int mode) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) q[i] = mode == 0 ? div_rn(a[i], b[i]) : mode == 1 ? __ddiv_rn(a[i], b[i]) : scalbn_rn(a[i], static_cast<int>(b[i]));
+}
+}  // namespace jsvd
+
+extern "C" jsvd_status jsvd_debug_primitive(int32_t mode, int64_t n, const double* a,
+                                            const double* b, double* q, void* stream) {
+  if (n < 0 || mode < 0 || mode > 2) return JSVD_EINVAL;
+  if (n == 0) return JSVD_OK;
+  jsvd::debug_div_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(n, a, b, q, mode);
+  jsvd::note_launch();
+  return cudaGetLastError() == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
+}

@@ -1,0 +1,273 @@
+// step_dev.cuh -- device building blocks of one Jacobi step (Alg 4.1 lines
+// 7-38) for a pivot pair held in registers by a CTA or a
+// thread-block cluster of CL CTAs x T threads (W = CL*T lanes).
+//
+// Reduction spec R (R#15): element i of a column lives in lane L = i mod W
+// (CTA rank L / T, thread L % T) and is accumulated in increasing i; lanes
+// combine by xor-butterfly over offsets [16,8,4,2,1] (warp shuffles), then the
+// warp-index bits high->low (shared memory), then the CTA-rank bits high->low
+// (distributed shared memory).  Addition is commutative, so every lane ends
+// with the identical total: the result depends only on (W, m), never on launch
+// geometry, scheduling or GPU count.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "jsvd_dev.cuh"
+
+namespace jsvd {
+namespace cg = cooperative_groups;
+
+constexpr int kIntMin = -2147483647 - 1;
+
+// ---------------------------------------------------------------- elements
+template <bool CPLX> struct Elem;
+template <> struct Elem<false> {
+  using T = double;
+  static __device__ __forceinline__ T zero() { return 0.0; }
+};
+template <> struct Elem<true> {
+  using T = double2;
+  static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+};
+
+__device__ __forceinline__ uint64_t absmax_bits(double x, uint64_t m) { return max(m, abs_bits(x)); }
+__device__ __forceinline__ uint64_t absmax_bits(double2 x, uint64_t m) {
+  return max(m, max(abs_bits(x.x), abs_bits(x.y)));
+}
+
+// 2^n for any n in [-1074, 1023]: normal or subnormal power of two, exact
+__device__ __forceinline__ double pow2_any(int n) {
+  return n >= -1022 ? pow2i(n) : __longlong_as_double(1ll << (n + 1074));
+}
+
+// x * 2^n with one rounding for n in [-1074, 2046] (R#3): one multiply, or two
+// when n > 1023 (the first, an upscaling, is exact).
+struct Pow2 {
+  double a, b;
+  bool two;
+  __device__ __forceinline__ explicit Pow2(int n) {
+    two = n > 1023;
+    a = two ? 0x1p1023 : pow2_any(n);
+    b = two ? pow2i(n - 1023) : 1.0;
+  }
+  __device__ __forceinline__ double operator()(double x) const { return two ? (x * a) * b : x * a; }
+  __device__ __forceinline__ double2 operator()(double2 x) const {
+    return make_double2((*this)(x.x), (*this)(x.y));
+  }
+};
+
+// ---------------------------------------------------------------- reductions
+// Fold s[0..N) by offsets N/2, ..., 1 keeping lane 0's view of the butterfly.
+template <int N, typename V, typename Op>
+__device__ __forceinline__ V fold(const V* s, Op op) {
+  V t[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) t[k] = s[k];
+#pragma unroll
+  for (int h = N / 2; h >= 1; h /= 2) {
+#pragma unroll
+    for (int k = 0; k < h; ++k) t[k] = op(t[k], t[k + h]);
+  }
+  return t[0];
+}
+
+struct AddOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return a + b; }
+};
+struct MaxIOp {
+  __device__ __forceinline__ int operator()(int a, int b) const { return max(a, b); }
+};
+struct MaxU64Op {
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const { return max(a, b); }
+};
+
+// Shared-memory slots of one 2-value reduction.
+template <int NW, typename V> struct RedSlot {
+  V warp[2][NW];
+  V cta[2];
+};
+
+// Sum of (a, b) over all W lanes in the order of R; every thread gets the result.
+template <int T, int CL>
+__device__ __forceinline__ void tree_sum2(double& a, double& b, RedSlot<T / 32, double>& s) {
+  constexpr int NW = T / 32;
+#pragma unroll
+  for (int o = 16; o >= 1; o /= 2) {
+    a = a + __shfl_xor_sync(0xffffffffu, a, o);
+    b = b + __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s.warp[0][w] = a;
+    s.warp[1][w] = b;
+  }
+  __syncthreads();
+  a = fold<NW>(s.warp[0], AddOp());
+  b = fold<NW>(s.warp[1], AddOp());
+  if constexpr (CL > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) {
+      s.cta[0] = a;
+      s.cta[1] = b;
+    }
+    cl.sync();
+    double ra[CL], rb[CL];
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const double* rs = cl.map_shared_rank(s.cta, r);
+      ra[r] = rs[0];
+      rb[r] = rs[1];
+    }
+    a = fold<CL>(ra, AddOp());
+    b = fold<CL>(rb, AddOp());
+  }
+}
+
+// Max of two ints over all W lanes (exact, order-free).
+template <int T, int CL>
+__device__ __forceinline__ void tree_max2i(int& a, int& b, RedSlot<T / 32, int>& s) {
+  constexpr int NW = T / 32;
+  a = __reduce_max_sync(0xffffffffu, a);
+  b = __reduce_max_sync(0xffffffffu, b);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s.warp[0][w] = a;
+    s.warp[1][w] = b;
+  }
+  __syncthreads();
+  a = fold<NW>(s.warp[0], MaxIOp());
+  b = fold<NW>(s.warp[1], MaxIOp());
+  if constexpr (CL > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) {
+      s.cta[0] = a;
+      s.cta[1] = b;
+    }
+    cl.sync();
+    int ra[CL], rb[CL];
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const int* rs = cl.map_shared_rank(s.cta, r);
+      ra[r] = rs[0];
+      rb[r] = rs[1];
+    }
+    a = fold<CL>(ra, MaxIOp());
+    b = fold<CL>(rb, MaxIOp());
+  }
+}
+
+// CTA-wide max of a u64 (result valid in thread 0 only).
+template <int T>
+__device__ __forceinline__ uint64_t cta_max_u64(uint64_t v, uint64_t* warp_slots) {
+#pragma unroll
+  for (int o = 16; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) warp_slots[threadIdx.x >> 5] = v;
+  __syncthreads();
+  return fold<T / 32>(warp_slots, MaxU64Op());
+}
+
+// floor(lg max|x|) of the lane's elements as an int (kIntMin if all zero)
+__device__ __forceinline__ int ilogb_or_min(uint64_t b) { return b ? ilogb_bits(b) : kIntMin; }
+
+// (e, f) of a column from E = floor(lg max) and the total SSQ of x 2^-E
+// (R#14): k = logb(SSQ), g = SSQ 2^-k, odd k -> (2g, k-1),
+// f = sqrt(g), e = E + k/2.  SSQ >= 1 here (the max element scales to [1,2)).
+__device__ __forceinline__ void ef_from_ssq(int E, double ssq, double& e, double& f) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(ssq));
+  int k = static_cast<int>(b >> 52) - 1023;
+  double g = __longlong_as_double(static_cast<long long>((b & 0x000fffffffffffffull) |
+                                                         0x3ff0000000000000ull));
+  if (k & 1) {
+    g = g * 2.0;
+    k -= 1;
+  }
+  f = __dsqrt_rn(g);
+  e = static_cast<double>(E + k / 2);
+}
+
+// fold one element into the SSQ accumulator (fma(y,y,.) re then im)
+__device__ __forceinline__ double ssq_acc(double y, double acc) { return fma(y, y, acc); }
+__device__ __forceinline__ double ssq_acc(double2 y, double acc) {
+  acc = fma(y.x, y.x, acc);
+  return fma(y.y, y.y, acc);
+}
+
+// Alg 3.1 lines 5-6: accumulate conj(q) p of prescaled elements
+__device__ __forceinline__ void dot_acc(double q, double p, double& ar, double&) {
+  ar = fma(q, p, ar);
+}
+__device__ __forceinline__ void dot_acc(double2 q, double2 p, double& ar, double& ai) {
+  ar = fma(q.x, p.x, ar);
+  ai = fma(q.x, p.y, ai);
+  ar = fma(q.y, p.y, ar);
+  ai = fma(-q.y, p.x, ai);
+}
+
+// Alg 3.4 with P = I: x_p' = fma(x_q, e', x_p) c, x_q' = fma(x_p, -conj(e'), x_q) c
+__device__ __forceinline__ void rot_elem(double& xp, double& xq, double c, double C, double) {
+  const double p = xp, q = xq;
+  xp = fma(q, C, p) * c;
+  xq = fma(p, -C, q) * c;
+}
+__device__ __forceinline__ void rot_elem(double2& xp, double2& xq, double c, double C, double S) {
+  const double rp = xp.x, ip = xp.y, rq = xq.x, iq = xq.y;
+  xp.x = fma(rq, C, fma(-iq, S, rp)) * c;
+  xp.y = fma(rq, S, fma(iq, C, ip)) * c;
+  xq.x = fma(rp, -C, fma(-ip, S, rq)) * c;
+  xq.y = fma(rp, S, fma(ip, -C, iq)) * c;
+}
+
+// getmant(x, [1,2), sign zero) and logb for a positive finite normal x
+__device__ __forceinline__ int ilogb_pos(double x) { return ilogb_bits(abs_bits(x)); }
+__device__ __forceinline__ double mant12(double x) {
+  const uint64_t b = abs_bits(x);
+  if (b >> 52) return __longlong_as_double(static_cast<long long>((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
+  return scalbn_rn(__longlong_as_double(static_cast<long long>(b)), -ilogb_bits(b));
+}
+
+// Alg 3.3: the non-overflowing scaled Grammian of the pair
+__device__ __forceinline__ void gram(double zr, double zi, double e1, double f1, double e2,
+                                     double f2, double& a11, double& a22, double& br, double& bi) {
+  double f12 = f1 / f2, e12 = e1 - e2;
+  double f21 = f2 / f1, e21 = e2 - e1;
+  e12 = e12 + static_cast<double>(ilogb_pos(f12));
+  f12 = mant12(f12);
+  e21 = e21 + static_cast<double>(ilogb_pos(f21));
+  f21 = mant12(f21);
+  const double sA = fmin(static_cast<double>(kEtaHat) - fmax(e12, e21), 0.0);
+  e12 = e12 + sA;
+  e21 = e21 + sA;
+  a11 = scalbn_rn(f12, static_cast<int>(e12));
+  a22 = scalbn_rn(f21, static_cast<int>(e21));
+  br = scalbn_rn(zr, static_cast<int>(sA));
+  bi = scalbn_rn(zi, static_cast<int>(sA));
+}
+
+// ---------------------------------------------------------------- strategy
+// R#20: circle method on P players, round r: position 0 = player 0, position
+// k >= 1 = player ((k-1+r) mod (P-1)) + 1; pair i = positions (i, P-1-i).
+__device__ __host__ __forceinline__ int circle_player(int64_t P, int64_t r, int64_t pos) {
+  return pos == 0 ? 0 : static_cast<int>((pos - 1 + r) % (P - 1)) + 1;
+}
+
+// pair l of step `step` of the block round-robin with B blocks of b = n/B
+__device__ __host__ __forceinline__ void strategy_pair(int64_t n, int64_t B, int64_t step,
+                                                       int64_t l, int& p, int& q) {
+  const int64_t b = n / B;
+  int64_t x, y;
+  if (step < b - 1) {  // phase I: flat RR inside every block
+    const int64_t beta = l / (b / 2), i = l % (b / 2);
+    x = beta * b + circle_player(b, step, i);
+    y = beta * b + circle_player(b, step, b - 1 - i);
+  } else {  // phase II: rounds of flat RR over blocks, b steps per round
+    const int64_t s2 = step - (b - 1), rr = s2 / b, tt = s2 % b;
+    const int64_t i = l / b, j = l % b;
+    const int64_t be = circle_player(B, rr, i), bf = circle_player(B, rr, B - 1 - i);
+    x = be * b + j;
+    y = bf * b + (j + tt) % b;
+  }
+  p = static_cast<int>(x < y ? x : y);
+  q = static_cast<int>(x < y ? y : x);
+}
+
+}  // namespace jsvd

@@ -1,0 +1,83 @@
+"""GPU primitive tests (layer 2): the device division and scalbn
+used by every kernel must equal IEEE binary64 RN arithmetic bit for bit,
+including zeros, subnormals, overflow and 0/0."""
+import ctypes as ct
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(mode, a, b):
+    import paper_2202_08361_b200 as J
+    L = J.lib()
+    L.jsvd_debug_primitive.restype = ct.c_int
+    L.jsvd_debug_primitive.argtypes = [ct.c_int32, ct.c_int64, ct.c_void_p, ct.c_void_p,
+                                       ct.c_void_p, ct.c_void_p]
+    ga, gb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    q = torch.empty_like(ga)
+    assert L.jsvd_debug_primitive(mode, a.size, ct.c_void_p(ga.data_ptr()),
+                                  ct.c_void_p(gb.data_ptr()), ct.c_void_p(q.data_ptr()), None) == 0
+    torch.cuda.synchronize()
+    return q.cpu().numpy()
+
+
+def _rand_doubles(rng, n):
+    """random sign/exponent/significand over the full finite range, incl. subnormals and 0"""
+    e = rng.integers(0, 2047, n, dtype=np.uint64)  # biased exponent 0..2046
+    m = rng.integers(0, 1 << 52, n, dtype=np.uint64)
+    s = rng.integers(0, 2, n, dtype=np.uint64) << np.uint64(63)
+    x = (s | (e << np.uint64(52)) | m).view(np.float64)
+    x[rng.random(n) < 0.02] = 0.0
+    return x
+
+
+def _same(q, ref):
+    qb, rb = q.view(np.uint64), ref.view(np.uint64)
+    nan = np.isnan(ref)
+    assert np.isnan(q[nan]).all()
+    bad = np.nonzero((qb != rb) & ~nan)[0]
+    return bad
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_division_full_range(seed):
+    rng = np.random.default_rng(seed)
+    n = 1 << 22
+    a, b = _rand_doubles(rng, n), _rand_doubles(rng, n)
+    with np.errstate(all="ignore"):
+        ref = a / b
+    for mode in (0, 1):
+        bad = _same(_run(mode, a, b), ref)
+        assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
+
+
+def test_division_near_underflow_and_overflow():
+    # quotients straddling the subnormal range and DBL_MAX, incl. exact ties
+    rng = np.random.default_rng(7)
+    n = 1 << 22
+    b = (1 + rng.random(n)) * 2.0 ** rng.integers(-60, 60, n)
+    target = rng.integers(-1080, -1015, n)
+    q0 = (1 + rng.random(n)) * 2.0 ** 0
+    a = np.ldexp(q0, target) * b
+    a2 = np.ldexp(rng.integers(1, 1 << 20, n).astype(float), -1074) * 3.0  # exact multiples
+    b2 = np.full(n, 3.0)
+    hi = (1 + rng.random(n)) * 2.0 ** rng.integers(1015, 1023, n)
+    lo = (1 + rng.random(n)) * 2.0 ** rng.integers(-12, 2, n)
+    for x, y in ((a, b), (a2, b2), (hi, lo), (np.ldexp(np.ones(n), -1074), 1 + rng.random(n))):
+        with np.errstate(all="ignore"):
+            ref = x / y
+        bad = _same(_run(0, x, y), ref)
+        assert bad.size == 0, (x[bad[:4]], y[bad[:4]])
+
+
+def test_scalbn_full_range():
+    rng = np.random.default_rng(11)
+    n = 1 << 22
+    a = _rand_doubles(rng, n)
+    k = rng.integers(-2200, 2200, n)
+    ref = np.ldexp(a, k)
+    bad = _same(_run(2, a, k.astype(np.float64)), ref)
+    assert bad.size == 0, (a[bad[:4]], k[bad[:4]])
