@@ -1,0 +1,391 @@
+// step.cu -- jsvd_sweep_step and the per-step kernel of jsvd_gesvj:
+// one parallel step of the one-sided Jacobi SVD (Alg 4.1 lines 7-38,
+// P:1530-1583) with s = 1 (R#13) and P = I (R#20).
+//
+// One pivot pair per CTA, or per thread-block cluster of CL CTAs when the
+// columns are long (DSMEM carries the cross-CTA reductions).  The pair's two
+// columns are loaded ONCE into registers (lane L = i mod W holds rows L, L+W,
+// ...: coalesced 8/16-byte loads), and every phase of the step runs on them:
+//   spade  column norms: exponent max, then SSQ of x 2^-E        (R#14)
+//   club   scaled dot a21' = g_q^* g_p (Alg 3.1)
+//   heart  convergence test (Alg 3.2), Grammian (Alg 3.3)     -- warp 0
+//   diam.  2x2 EVD (Alg 2.2, TAN|NOBACKSCALE)                 -- warp 0
+//   star   rotation of g_p, g_q in registers + store, then v_p, v_q (Alg 3.4)
+// so G is read once and written once per transformed pair, V read+written
+// once per transformed pair, nothing for a converged pair (R#26: no max on V).
+#include "jsvd_host.h"
+#include "step_dev.cuh"
+#include "step_params.h"
+
+namespace jsvd {
+
+template <bool CPLX, int T, int CL, int NR>
+__global__ void __launch_bounds__(T) step_kernel(const StepParams P) {
+  using E = typename Elem<CPLX>::T;
+  constexpr int W = T * CL;
+  constexpr int NW = T / 32;
+  __shared__ RedSlot<NW, int> rs_e;
+  __shared__ RedSlot<NW, double> rs_ssq;
+  __shared__ RedSlot<NW, double> rs_dot;
+  __shared__ uint64_t rs_m[NW];
+  __shared__ double rot[3];
+
+  const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
+  const int64_t pair = blockIdx.x / CL;
+  int p, q;
+  if (P.pairs) {
+    p = P.pairs[2 * pair];
+    q = P.pairs[2 * pair + 1];
+  } else {
+    strategy_pair(P.n, P.B, P.step, pair, p, q);
+  }
+  const int L = crank * T + static_cast<int>(threadIdx.x);
+  E* gp = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(p) * P.ldg;
+  E* gq = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(q) * P.ldg;
+  const bool lead = (crank == 0) && (threadIdx.x == 0);
+
+  // rescale check (Alg 4.1 line 6; Eqs. skn/skr; R#21): every step touches all
+  // n columns, so each pair scales its own two columns on load.
+  int sn = 0;
+  uint64_t mt_cur = 0;
+  if (P.Mt) {
+    mt_cur = P.Mt[P.slot];
+    if (P.checkpoint) {
+      const int lm = ilogb_bits(mt_cur);
+      if (P.Kr - lm < 0) sn = P.Fm - lm - 1;
+    }
+  }
+
+  E xp[NR], xq[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int64_t i = static_cast<int64_t>(j) * W + L;
+    if (i < P.m) {
+      xp[j] = gp[i];
+      xq[j] = gq[i];
+    } else {
+      xp[j] = Elem<CPLX>::zero();
+      xq[j] = Elem<CPLX>::zero();
+    }
+  }
+  if (sn != 0) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      if constexpr (CPLX) {
+        xp[j] = make_double2(scalbn_rn(xp[j].x, sn), scalbn_rn(xp[j].y, sn));
+        xq[j] = make_double2(scalbn_rn(xq[j].x, sn), scalbn_rn(xq[j].y, sn));
+      } else {
+        xp[j] = scalbn_rn(xp[j], sn);
+        xq[j] = scalbn_rn(xq[j], sn);
+      }
+    }
+  }
+
+  // ---- spade: E = floor(lg max |component|) per column
+  uint64_t mp = 0, mq = 0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    mp = absmax_bits(xp[j], mp);
+    mq = absmax_bits(xq[j], mq);
+  }
+  int Ep = ilogb_or_min(mp), Eq = ilogb_or_min(mq);
+  tree_max2i<T, CL>(Ep, Eq, rs_e);
+  // ---- spade: SSQ of x 2^-E in the lane order of R
+  double sp = 0.0, sq = 0.0;
+  if (Ep != kIntMin) {
+    const Pow2 f(-Ep);
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      if (static_cast<int64_t>(j) * W + L < P.m) sp = ssq_acc(f(xp[j]), sp);
+  }
+  if (Eq != kIntMin) {
+    const Pow2 f(-Eq);
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      if (static_cast<int64_t>(j) * W + L < P.m) sq = ssq_acc(f(xq[j]), sq);
+  }
+  tree_sum2<T, CL>(sp, sq, rs_ssq);
+  double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
+  if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
+  if (Eq != kIntMin) ef_from_ssq(Eq, sq, eq, fq);
+  if (lead) {
+    P.col_e[p] = ep;
+    P.col_f[p] = fp;
+    P.col_e[q] = eq;
+    P.col_f[q] = fq;
+  }
+
+  // ---- club: a21' = (g_q 2^-e_q)^* (g_p 2^-e_p) / fl(f_q f_p)  (Alg 3.1)
+  double zr = 0.0, zi = 0.0;
+  const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19
+  if (!zero_col) {
+    const Pow2 fP(-static_cast<int>(ep)), fQ(-static_cast<int>(eq));
+    double ar = 0.0, ai = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      if (static_cast<int64_t>(j) * W + L < P.m) dot_acc(fQ(xq[j]), fP(xp[j]), ar, ai);
+    tree_sum2<T, CL>(ar, ai, rs_dot);
+    const Divisor d = make_divisor(fq * fp);
+    zr = divide(ar, d);
+    zi = CPLX ? divide(ai, d) : 0.0;
+  }
+  // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
+  const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
+  const bool transform = P.tol <= az;
+
+  uint64_t Mloc = 0;
+  if (transform) {
+    if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
+      double b11, b22, br, bi;
+      gram(zr, zi, ep, fp, eq, fq, b11, b22, br, bi);
+      const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi);
+      if (threadIdx.x == 0) {
+        rot[0] = o.c;
+        rot[1] = o.sr;
+        rot[2] = o.si;
+      }
+    }
+    __syncthreads();
+    const double c = rot[0], C = rot[1], S = rot[2];
+    // ---- star: rotate the register-resident pair, track max |component|
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      rot_elem(xp[j], xq[j], c, C, S);
+      Mloc = absmax_bits(xp[j], Mloc);
+      Mloc = absmax_bits(xq[j], Mloc);
+    }
+  }
+  if (transform || sn != 0) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int64_t i = static_cast<int64_t>(j) * W + L;
+      if (i < P.m) {
+        gp[i] = xp[j];
+        gq[i] = xq[j];
+      }
+    }
+  }
+  if (transform) {
+    if (P.V) {
+      const double c = rot[0], C = rot[1], S = rot[2];
+      E* vp = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(p) * P.ldv;
+      E* vq = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(q) * P.ldv;
+      for (int64_t i = L; i < P.n; i += W) {
+        E a = vp[i], b = vq[i];
+        rot_elem(a, b, c, C, S);
+        vp[i] = a;
+        vq[i] = b;
+      }
+    }
+    const uint64_t Mc = cta_max_u64<T>(Mloc, rs_m);
+    if (threadIdx.x == 0) {
+      atomicMax(P.Mt ? &P.Mt[(P.slot + 1) % 3] : P.mmax, static_cast<unsigned long long>(Mc));
+      if (crank == 0) atomicAdd(P.t_dev, 1ull);
+    }
+  }
+  if (P.Mt && pair == 0 && lead) {  // M-tilde / s bookkeeping for the next step
+    const double cur = __longlong_as_double(static_cast<long long>(mt_cur));
+    const double scaled = sn ? scalbn_rn(cur, sn) : cur;
+    atomicMax(&P.Mt[(P.slot + 1) % 3],
+              static_cast<unsigned long long>(__double_as_longlong(scaled)));
+    P.Mt[(P.slot + 2) % 3] = 0ull;
+    P.s_slots[(P.slot + 1) % 3] = P.s_slots[P.slot] + sn;
+  }
+  if constexpr (CL > 1) cg::this_cluster().sync();  // keep DSMEM alive for peers
+}
+
+// ---- finalize helpers ---------------------------------------
+// norms of all columns with the same code and lane order as the step (R#23)
+template <bool CPLX, int T, int CL, int NR>
+__global__ void __launch_bounds__(T) colnorm_kernel(int64_t m, const double* G, int64_t ldg,
+                                                    double* col_e, double* col_f) {
+  using E = typename Elem<CPLX>::T;
+  constexpr int W = T * CL;
+  constexpr int NW = T / 32;
+  __shared__ RedSlot<NW, int> rs_e;
+  __shared__ RedSlot<NW, double> rs_ssq;
+  const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
+  const int64_t col = blockIdx.x / CL;
+  const int L = crank * T + static_cast<int>(threadIdx.x);
+  const E* g = reinterpret_cast<const E*>(G) + col * ldg;
+  E x[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int64_t i = static_cast<int64_t>(j) * W + L;
+    x[j] = i < m ? g[i] : Elem<CPLX>::zero();
+  }
+  uint64_t mx = 0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) mx = absmax_bits(x[j], mx);
+  int Ex = ilogb_or_min(mx), dummy = kIntMin;
+  tree_max2i<T, CL>(Ex, dummy, rs_e);
+  double s = 0.0, s2 = 0.0;
+  if (Ex != kIntMin) {
+    const Pow2 f(-Ex);
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      if (static_cast<int64_t>(j) * W + L < m) s = ssq_acc(f(x[j]), s);
+  }
+  tree_sum2<T, CL>(s, s2, rs_ssq);
+  double e = -INFINITY, f = 1.0;
+  if (Ex != kIntMin) ef_from_ssq(Ex, s, e, f);
+  if (crank == 0 && threadIdx.x == 0) {
+    col_e[col] = e;
+    col_f[col] = f;
+  }
+  if constexpr (CL > 1) cg::this_cluster().sync();
+}
+
+// ---- geometry --------------------------------------------------------------
+struct Geo {
+  int T, CL, NR;
+};
+
+static Geo pick_geo(bool cplx, int64_t m) {
+  const int NR = cplx ? 8 : 16;  // register-resident elements per lane and column
+  int64_t need = (m + NR - 1) / NR, W = 256;
+  while (W < need) W *= 2;
+  if (W > 4096) return Geo{0, 0, 0};
+  const int T = static_cast<int>(W < 512 ? W : 512);
+  return Geo{T, static_cast<int>(W / T), NR};
+}
+
+template <typename Kern, typename... Args>
+static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(T);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  note_launch();
+  return e;
+}
+
+template <bool CPLX>
+static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams& P,
+                                 cudaStream_t st) {
+  constexpr int NR = CPLX ? 8 : 16;
+  const int64_t grid = npairs * g.CL;
+  if (g.T == 256) return launch_cl(step_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, P);
+  switch (g.CL) {
+    case 1: return launch_cl(step_kernel<CPLX, 512, 1, NR>, grid, 512, 1, st, P);
+    case 2: return launch_cl(step_kernel<CPLX, 512, 2, NR>, grid, 512, 2, st, P);
+    case 4: return launch_cl(step_kernel<CPLX, 512, 4, NR>, grid, 512, 4, st, P);
+    case 8: return launch_cl(step_kernel<CPLX, 512, 8, NR>, grid, 512, 8, st, P);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_step(bool cplx, int64_t npairs, const StepParams& P, cudaStream_t st) {
+  const Geo g = pick_geo(cplx, P.m);
+  return cplx ? launch_step_t<true>(g, npairs, P, st) : launch_step_t<false>(g, npairs, P, st);
+}
+
+template <bool CPLX>
+static cudaError_t launch_colnorm_t(const Geo& g, int64_t m, int64_t n, const double* G,
+                                    int64_t ldg, double* ce, double* cf, cudaStream_t st) {
+  constexpr int NR = CPLX ? 8 : 16;
+  const int64_t grid = n * g.CL;
+  if (g.T == 256) return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, m, G, ldg, ce, cf);
+  switch (g.CL) {
+    case 1: return launch_cl(colnorm_kernel<CPLX, 512, 1, NR>, grid, 512, 1, st, m, G, ldg, ce, cf);
+    case 2: return launch_cl(colnorm_kernel<CPLX, 512, 2, NR>, grid, 512, 2, st, m, G, ldg, ce, cf);
+    case 4: return launch_cl(colnorm_kernel<CPLX, 512, 4, NR>, grid, 512, 4, st, m, G, ldg, ce, cf);
+    case 8: return launch_cl(colnorm_kernel<CPLX, 512, 8, NR>, grid, 512, 8, st, m, G, ldg, ce, cf);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_colnorm(bool cplx, int64_t m, int64_t n, const double* G, int64_t ldg,
+                           double* ce, double* cf, cudaStream_t st) {
+  const Geo g = pick_geo(cplx, m);
+  return cplx ? launch_colnorm_t<true>(g, m, n, G, ldg, ce, cf, st)
+              : launch_colnorm_t<false>(g, m, n, G, ldg, ce, cf, st);
+}
+
+bool step_supported(bool cplx, int64_t m) { return pick_geo(cplx, m).T != 0; }
+
+__global__ void strategy_kernel(int64_t n, int64_t B, int64_t step, int32_t* pairs) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l < n / 2) {
+    int p, q;
+    strategy_pair(n, B, step, l, p, q);
+    pairs[2 * l] = p;
+    pairs[2 * l + 1] = q;
+  }
+}
+
+bool strategy_ok(int64_t n, int64_t B) {
+  if (n < 2 || (n & 1) || B < 2 || n % B) return false;
+  const int64_t b = n / B;
+  return b == 1 || (b % 2) == 0;
+}
+
+}  // namespace jsvd
+
+using namespace jsvd;
+
+extern "C" jsvd_status jsvd_step_rspec(jsvd_dtype dt, int64_t m, int32_t* W, int32_t* c,
+                                       int32_t* offs, int32_t* noffs) {
+  if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || !W || !c || !offs || !noffs)
+    return JSVD_EINVAL;
+  const Geo g = pick_geo(dt == JSVD_C64, m);
+  if (!g.T) return JSVD_EINVAL;
+  *W = g.T * g.CL;
+  *c = 1;
+  int k = 0;
+  for (int o = 16; o >= 1; o /= 2) offs[k++] = o;
+  for (int o = g.T / 2; o >= 32; o /= 2) offs[k++] = o;
+  for (int o = g.T * g.CL / 2; o >= g.T; o /= 2) offs[k++] = o;
+  *noffs = k;
+  return JSVD_OK;
+}
+
+extern "C" jsvd_status jsvd_strategy_pairs(int64_t n, int32_t nblocks, int64_t step,
+                                           int32_t* pairs, void* stream) {
+  if (!strategy_ok(n, nblocks) || step < 0 || step >= n - 1 || !pairs) return JSVD_EINVAL;
+  const int64_t np = n / 2;
+  strategy_kernel<<<static_cast<unsigned>((np + 255) / 256), 256, 0,
+                    static_cast<cudaStream_t>(stream)>>>(n, nblocks, step, pairs);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
+}
+
+static double upsilon_host(int64_t m) { return std::ldexp(std::sqrt(static_cast<double>(m)), -53); }
+
+extern "C" jsvd_status jsvd_sweep_step(jsvd_dtype dt, int64_t m, int64_t n, double* G, int64_t ldg,
+                                       double* V, int64_t ldv, const int32_t* pairs,
+                                       int64_t npairs, double tol, double* col_e, double* col_f,
+                                       int64_t* t_dev, double* mmax_dev, void* stream) {
+  const bool cplx = dt == JSVD_C64;
+  if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || n < 2 || ldg < m || !G || !pairs ||
+      npairs < 0 || npairs > n / 2 || !col_e || !col_f || !t_dev || !mmax_dev)
+    return JSVD_EINVAL;
+  if (V && ldv < n) return JSVD_EINVAL;
+  if (!step_supported(cplx, m)) return JSVD_EINVAL;
+  if (cplx && ((reinterpret_cast<uintptr_t>(G) & 15) || (V && (reinterpret_cast<uintptr_t>(V) & 15))))
+    return JSVD_EINVAL;
+  if (npairs == 0) return JSVD_OK;
+  StepParams P{};
+  P.m = m;
+  P.n = n;
+  P.G = G;
+  P.ldg = ldg;
+  P.V = V;
+  P.ldv = ldv;
+  P.pairs = pairs;
+  P.tol = tol > 0.0 ? tol : upsilon_host(m);
+  P.col_e = col_e;
+  P.col_f = col_f;
+  P.t_dev = reinterpret_cast<unsigned long long*>(t_dev);
+  P.mmax = reinterpret_cast<unsigned long long*>(mmax_dev);
+  cudaError_t e = launch_step(cplx, npairs, P, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
+}

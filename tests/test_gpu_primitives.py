@@ -73,6 +73,29 @@ def test_division_near_underflow_and_overflow():
         assert bad.size == 0, (x[bad[:4]], y[bad[:4]])
 
 
+def test_division_structured_significands():
+    # all-ones / all-zeros / single-bit significands of both operands, every
+    # combination, at exponent offsets around the normal/subnormal boundary
+    sig = [1.0, 2.0 - 2.0 ** -52, 1.5, 1.0 + 2.0 ** -52, 1.5 - 2.0 ** -52, 1.25, 1.75 + 2.0 ** -52,
+           1.0 + 2.0 ** -26, 2.0 - 2.0 ** -26, 1.3333333333333333, 1.6666666666666667]
+    rng = np.random.default_rng(3)
+    sig += list(1 + rng.random(40))
+    ea = [-1074, -1060, -1030, -1023, -1022, -1000, -500, -3, 0, 1, 500, 1000, 1021, 1023]
+    A, B = [], []
+    for a in sig:
+        for b in sig:
+            for x in ea:
+                for y in ea:
+                    A.append(np.ldexp(a, x))
+                    B.append(np.ldexp(b, y))
+    a, b = np.array(A), np.array(B)
+    with np.errstate(all="ignore"):
+        ref = a / b
+    for mode in (0, 1):
+        bad = _same(_run(mode, a, b), ref)
+        assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
+
+
 def test_scalbn_full_range():
     rng = np.random.default_rng(11)
     n = 1 << 22

@@ -1,0 +1,161 @@
+"""GPU parity of the Jacobi-SVD entry points against the oracle, BITWISE:
+jsvd_strategy_pairs, jsvd_sweep_step (every kernel geometry: single CTA and
+2/4/8-CTA clusters), jsvd_gesvj (U, V, sigma, (e,f), sweeps, T per sweep).
+The oracle is given the reduction spec R the library reports for (dtype, m)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def J():
+    import paper_2202_08361_b200 as J
+    assert torch.cuda.is_available()
+    return J
+
+
+def rspec(J, cplx, m):
+    W, c, offs = J.step_rspec(cplx, m)
+    return O.RSpec.make(W, c, offs)
+
+
+def colmajor_gpu(A):
+    t = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()  # (n, m) row-major == (m, n) col-major
+    return t.T
+
+
+def to_np(t):
+    return t.T.contiguous().cpu().numpy().T
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if np.iscomplexobj(a):
+        a, b = a.view(np.float64), b.view(np.float64)
+    return np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,B", [(2, 2), (8, 8), (8, 2), (16, 4), (64, 16), (1024, 1024),
+                                 (1024, 16), (96, 6)])
+def test_strategy_pairs_match_oracle(J, n, B):
+    for k in range(n - 1):
+        g = J.strategy_pairs(n, B, k).cpu().numpy()
+        assert np.array_equal(g, O.strategy_pairs(n, B, k)), (n, B, k)
+
+
+def _scaled_input(rng, m, n, cplx, specials=True):
+    A = rng.standard_normal((m, n)) * 2.0 ** rng.integers(-40, 40, n)
+    if cplx:
+        A = A + 1j * rng.standard_normal((m, n)) * 2.0 ** rng.integers(-40, 40, n)
+    if specials and n >= 6:
+        A[:, 1] = 0.0                                 # zero column (R#19)
+        A[: max(1, m // 3), 2] = 5e-324 * 3           # subnormal entries
+        A[:, 3] *= 2.0 ** -1000                       # tiny column
+        A[:, 4] *= 2.0 ** 600                         # huge relative range
+    # the step's precondition: pre-scaled as jsvd_gesvj would (||G||max <= omega/(4m))
+    mx = np.abs(A.view(np.float64) if cplx else A).max()
+    s = O.Fm(cplx, m) - int(np.floor(np.log2(mx))) - 1
+    return np.asfortranarray(np.ldexp(A.real, s) + (1j * np.ldexp(A.imag, s) if cplx else 0))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("m", [1, 7, 64, 255, 256, 257, 1000, 2049, 4096, 8191, 16384, 32768])
+def test_sweep_step_bitwise(J, cplx, m):
+    if not cplx and m == 32768:
+        m = 65536  # the real 8-CTA cluster geometry
+    n = 12
+    rng = np.random.default_rng(m + 7 * cplx)
+    A = _scaled_input(rng, m, n, cplx)
+    V = np.asfortranarray(np.eye(n, dtype=A.dtype) + 0.0)
+    R = rspec(J, cplx, m)
+    G_ref, V_ref = A.copy(order="F"), V.copy(order="F")
+    g, v = colmajor_gpu(A), colmajor_gpu(V)
+    for k in range(3):
+        pairs = O.strategy_pairs(n, n, k)
+        ref = O.step(G_ref, V_ref, pairs, R)
+        out = J.sweep_step(g, v, torch.from_numpy(pairs.astype(np.int32)).cuda())
+        torch.cuda.synchronize()
+        assert bits_equal(to_np(g), G_ref), (m, k)
+        assert bits_equal(to_np(v), V_ref), (m, k)
+        assert bits_equal(out["col_e"].cpu().numpy(), ref["col_e"])
+        assert bits_equal(out["col_f"].cpu().numpy(), ref["col_f"])
+        assert int(out["t"].item()) == ref["t"]
+        assert out["mmax"].item() == ref["mmax"]
+
+
+def test_sweep_step_partial_pairs_and_no_V(J):
+    m, n = 300, 10
+    rng = np.random.default_rng(3)
+    A = _scaled_input(rng, m, n, False, specials=False)
+    R = rspec(J, False, m)
+    pairs = np.array([[0, 9], [4, 2]], np.int32)  # p > q on purpose in the second pair? no: p<q
+    pairs = np.array([[0, 9], [2, 4]], np.int32)
+    G_ref = A.copy(order="F")
+    ref = O.step(G_ref, None, pairs, R)
+    g = colmajor_gpu(A)
+    out = J.sweep_step(g, None, torch.from_numpy(pairs).cuda())
+    torch.cuda.synchronize()
+    assert bits_equal(to_np(g), G_ref)
+    assert int(out["t"].item()) == ref["t"] == 2
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("m,n,B", [(8, 8, 8), (64, 32, 32), (100, 20, 20), (257, 16, 4),
+                                   (512, 64, 16), (600, 40, 40)])
+def test_gesvj_bitwise(J, cplx, m, n, B):
+    rng = np.random.default_rng(m * n + cplx)
+    A = rng.standard_normal((m, n)) * (2.0 ** -rng.integers(0, 30, n))
+    if cplx:
+        A = A + 1j * rng.standard_normal((m, n))
+    R = rspec(J, cplx, m)
+    ref = O.gesvj(A, R, B=B, max_sweeps=40)
+    g = colmajor_gpu(np.asfortranarray(A))
+    out = J.gesvj(g, nblocks=B, max_sweeps=40)
+    assert out["status"] == ref["status"]
+    assert out["sweeps"] == ref["sweeps"]
+    assert list(out["tps"]) == list(ref["tps"])
+    assert bits_equal(to_np(out["U"]), ref["U"])
+    assert bits_equal(to_np(out["V"]), ref["V"])
+    assert bits_equal(out["sigma"].cpu().numpy(), ref["sigma"])
+    assert bits_equal(out["sigma_e"].cpu().numpy(), ref["sigma_e"])
+    assert bits_equal(out["sigma_f"].cpu().numpy(), ref["sigma_f"])
+
+
+def test_gesvj_capped_run_and_errors(J):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((64, 16))
+    R = rspec(J, False, 64)
+    ref = O.gesvj(A, R, max_sweeps=2)
+    out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), max_sweeps=2)
+    assert out["status"] == ref["status"] == 1  # ENOCONV (R#25)
+    assert bits_equal(to_np(out["U"]), ref["U"])
+    with pytest.raises(J.JsvdError):
+        J.gesvj(colmajor_gpu(np.zeros((8, 4))))
+    bad = np.ones((8, 4))
+    bad[2, 2] = np.nan
+    with pytest.raises(J.JsvdError):
+        J.gesvj(colmajor_gpu(bad))
+
+
+def test_config3_full_size_step_bitwise(J):
+    # BASELINE configs[2] at full size (4096 x 1024): the first 3 steps of
+    # jsvd_gesvj's first sweep, GPU vs oracle, after the same initial scaling.
+    A, _ = synth.svd_cfg3()
+    m, n = A.shape
+    R = rspec(J, False, m)
+    s0 = O.Fm(False, m) - int(np.floor(np.log2(np.abs(A).max()))) - 1
+    G = np.asfortranarray(np.ldexp(A, s0))
+    V = np.asfortranarray(np.eye(n))
+    g, v = colmajor_gpu(G), colmajor_gpu(V)
+    for k in range(3):
+        pairs = O.strategy_pairs(n, n, k)
+        ref = O.step(G, V, pairs, R)
+        out = J.sweep_step(g, v, torch.from_numpy(pairs.astype(np.int32)).cuda())
+        torch.cuda.synchronize()
+        assert int(out["t"].item()) == ref["t"] == n // 2
+        assert bits_equal(to_np(g), G) and bits_equal(to_np(v), V)
