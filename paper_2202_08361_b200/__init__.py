@@ -19,7 +19,7 @@ import torch
 
 from ._build import LIB
 
-__all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "strategy_pairs", "gesvj",
+__all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
            "gesvj_workspace", "gesvj_batched", "launch_count", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
@@ -55,6 +55,8 @@ def lib():
         L.jsvd_step_rspec.restype = ct.c_int
         L.jsvd_step_rspec.argtypes = [ct.c_int, _i64] + [ct.POINTER(_i32)] * 2 + [_vp,
                                                                                    ct.POINTER(_i32)]
+        L.jsvd_batched_rspec.restype = ct.c_int
+        L.jsvd_batched_rspec.argtypes = L.jsvd_step_rspec.argtypes
         L.jsvd_strategy_pairs.restype = ct.c_int
         L.jsvd_strategy_pairs.argtypes = [_i64, _i32, _i64, _vp, _vp]
         L.jsvd_gesvj_workspace.restype = ct.c_int
@@ -140,6 +142,15 @@ def step_rspec(cplx, m):
     offs = (_i32 * 32)()
     _check(lib().jsvd_step_rspec(C64 if cplx else R64, m, ct.byref(W), ct.byref(c),
                                  ct.cast(offs, _vp), ct.byref(no)), "jsvd_step_rspec")
+    return W.value, c.value, tuple(offs[k] for k in range(no.value))
+
+
+def batched_rspec(cplx, m):
+    """(W, c, offsets) of jsvd_gesvj_batched's kernel."""
+    W, c, no = _i32(), _i32(), _i32()
+    offs = (_i32 * 32)()
+    _check(lib().jsvd_batched_rspec(C64 if cplx else R64, m, ct.byref(W), ct.byref(c),
+                                    ct.cast(offs, _vp), ct.byref(no)), "jsvd_batched_rspec")
     return W.value, c.value, tuple(offs[k] for k in range(no.value))
 
 

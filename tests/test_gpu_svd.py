@@ -159,3 +159,46 @@ def test_config3_full_size_step_bitwise(J):
         torch.cuda.synchronize()
         assert int(out["t"].item()) == ref["t"] == n // 2
         assert bits_equal(to_np(g), G) and bits_equal(to_np(v), V)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("m,n", [(2, 2), (8, 6), (64, 32), (33, 32), (100, 40), (128, 64)])
+def test_gesvj_batched_bitwise(J, cplx, m, n):
+    rng = np.random.default_rng(m + n + cplx)
+    b = 5
+    A = rng.standard_normal((b, m, n)) * 2.0 ** rng.integers(-20, 20, (b, 1, n))
+    if cplx:
+        A = A + 1j * rng.standard_normal((b, m, n))
+    A[1, :, 0] = 0.0  # a zero column
+    W, c, offs = J.batched_rspec(cplx, m)
+    ref = O.gesvj_batched(A, O.RSpec.make(W, c, offs), max_sweeps=40)
+    g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+    out = J.gesvj_batched(g, max_sweeps=40)
+    torch.cuda.synchronize()
+    assert np.array_equal(out["status"].cpu().numpy(), ref["status"])
+    assert np.array_equal(out["sweeps"].cpu().numpy(), ref["sweeps"])
+    U = out["U"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+    V = out["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+    assert bits_equal(U, ref["U"]) and bits_equal(V, ref["V"])
+    assert bits_equal(out["sigma"].cpu().numpy(), ref["sigma"])
+
+
+def test_config4_batched_sampled_bitwise(J):
+    # BASELINE configs[3] at full size in the bench's launch configuration
+    # (65536 x 64 x 32 complex, one CTA per matrix); the oracle checks a
+    # random sample of 64 matrices one by one.
+    bsz, m, n = 65536, 64, 32
+    A = synth.svd_cfg4(bsz)
+    g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+    out = J.gesvj_batched(g, max_sweeps=30)
+    torch.cuda.synchronize()
+    assert (out["status"] == 0).all()
+    idx = np.sort(np.random.default_rng(2).choice(bsz, 64, replace=False))
+    W, c, offs = J.batched_rspec(True, m)
+    ref = O.gesvj_batched(A[idx], O.RSpec.make(W, c, offs), max_sweeps=30)
+    U = out["U"][idx].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+    assert bits_equal(U, ref["U"])
+    assert bits_equal(out["sigma"][idx].cpu().numpy(), ref["sigma"])
+    # north_star tolerances on the GPU result: sigma vs LAPACK, residual, orthogonality
+    s = np.linalg.svd(A[idx], compute_uv=False)
+    assert (np.abs(out["sigma"][idx].cpu().numpy() - s) / s).max() <= 1e-12
