@@ -167,9 +167,10 @@ def _mat(t, name):
     if t.dtype not in (torch.float64, torch.complex128):
         raise ValueError(f"{name} must be float64 or complex128")
     m, n = t.shape
-    if t.stride(0) != 1 or (n > 1 and t.stride(1) < m):
+    ld = t.stride(1) if n > 1 else m
+    if (m > 1 and t.stride(0) != 1) or ld < m:
         raise ValueError(f"{name} must be column-major (use A.T.contiguous().T)")
-    return t.dtype == torch.complex128, max(t.stride(1), m) if n > 1 else m
+    return t.dtype == torch.complex128, ld
 
 
 def sweep_step(G, V, pairs, tol=0.0, col_e=None, col_f=None, t_dev=None, mmax_dev=None,

@@ -262,7 +262,8 @@ __device__ __host__ __forceinline__ void strategy_pair(int64_t n, int64_t B, int
   } else {  // phase II: rounds of flat RR over blocks, b steps per round
     const int64_t s2 = step - (b - 1), rr = s2 / b, tt = s2 % b;
     const int64_t i = l / b, j = l % b;
-    const int64_t be = circle_player(B, rr, i), bf = circle_player(B, rr, B - 1 - i);
+    const int64_t u = circle_player(B, rr, i), v = circle_player(B, rr, B - 1 - i);
+    const int64_t be = u < v ? u : v, bf = u < v ? v : u;  // block pair (beta < beta')
     x = be * b + j;
     y = bf * b + (j + tt) % b;
   }

@@ -34,7 +34,9 @@ def to_np(t):
 
 
 def bits_equal(a, b):
-    a, b = np.asarray(a), np.asarray(b)
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    if a.shape != b.shape:
+        return False
     if np.iscomplexobj(a):
         a, b = a.view(np.float64), b.view(np.float64)
     return np.array_equal(a.view(np.uint64), b.view(np.uint64))
