@@ -168,13 +168,23 @@ extern "C" jsvd_status jsvd_evd2_batched(jsvd_dtype dt, int64_t r, const double*
 namespace jsvd {
 __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, double* q, int mode) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) q[i] = mode == 0 ? div_rn(a[i], b[i]) : mode == 1 ? __ddiv_rn(a[i], b[i]) : scalbn_rn(a[i], static_cast<int>(b[i]));
+  if (i < n) {
+    const double x = a[i], y = b[i];
+    switch (mode) {
+      case 0: q[i] = div_rn(x, y); break;
+      case 1: q[i] = __ddiv_rn(x, y); break;
+      case 2: q[i] = scalbn_rn(x, static_cast<int>(y)); break;
+      case 3: q[i] = divide_sf(x, make_divisor(y)); break;
+      case 4: q[i] = divide_checked(x, make_divisor(y)); break;
+      default: q[i] = hypot_naive(fabs(x), fabs(y)); break;
+    }
+  }
 }
 }  // namespace jsvd
 
 extern "C" jsvd_status jsvd_debug_primitive(int32_t mode, int64_t n, const double* a,
                                             const double* b, double* q, void* stream) {
-  if (n < 0 || mode < 0 || mode > 2) return JSVD_EINVAL;
+  if (n < 0 || mode < 0 || mode > 5) return JSVD_EINVAL;
   if (n == 0) return JSVD_OK;
   jsvd::debug_div_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
                            static_cast<cudaStream_t>(stream)>>>(n, a, b, q, mode);

@@ -69,8 +69,9 @@ def test_division_near_underflow_and_overflow():
     for x, y in ((a, b), (a2, b2), (hi, lo), (np.ldexp(np.ones(n), -1074), 1 + rng.random(n))):
         with np.errstate(all="ignore"):
             ref = x / y
-        bad = _same(_run(0, x, y), ref)
-        assert bad.size == 0, (x[bad[:4]], y[bad[:4]])
+        for mode in (0, 3, 4):
+            bad = _same(_run(mode, x, y), ref)
+            assert bad.size == 0, (mode, x[bad[:4]], y[bad[:4]])
 
 
 def test_division_structured_significands():
@@ -91,9 +92,22 @@ def test_division_structured_significands():
     a, b = np.array(A), np.array(B)
     with np.errstate(all="ignore"):
         ref = a / b
-    for mode in (0, 1):
+    for mode in (0, 1, 3, 4):
         bad = _same(_run(mode, a, b), ref)
         assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
+
+
+def test_hypot_exact_shortcut_matches_oracle():
+    import oracle as O
+    rng = np.random.default_rng(21)
+    n = 1 << 16
+    x = np.abs(_rand_doubles(rng, n))
+    y = x * 2.0 ** rng.integers(-60, 60, n) * (1 + rng.random(n))
+    y[::7] = 0.0
+    g = _run(5, x, y)
+    ref = np.array([O.hypot(a, b) for a, b in zip(x, y)])
+    bad = _same(g, ref)
+    assert bad.size == 0, (x[bad[:4]], y[bad[:4]])
 
 
 def test_scalbn_full_range():
