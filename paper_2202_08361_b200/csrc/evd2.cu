@@ -174,9 +174,10 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
       case 0: q[i] = div_rn(x, y); break;
       case 1: q[i] = __ddiv_rn(x, y); break;
       case 2: q[i] = scalbn_rn(x, static_cast<int>(y)); break;
-      case 3: q[i] = divide_sf(x, make_divisor(y)); break;
+      case 3: q[i] = divide_sf<true, true>(x, make_divisor(y)); break;
       case 4: q[i] = divide_checked(x, make_divisor(y)); break;
-      default: q[i] = hypot_naive(fabs(x), fabs(y)); break;
+      case 5: q[i] = hypot_naive(fabs(x), fabs(y)); break;
+      default: q[i] = divide_sf<false, true>(x, make_divisor(y)); break;
     }
   }
 }
@@ -184,7 +185,7 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
 
 extern "C" jsvd_status jsvd_debug_primitive(int32_t mode, int64_t n, const double* a,
                                             const double* b, double* q, void* stream) {
-  if (n < 0 || mode < 0 || mode > 5) return JSVD_EINVAL;
+  if (n < 0 || mode < 0 || mode > 6) return JSVD_EINVAL;
   if (n == 0) return JSVD_OK;
   jsvd::debug_div_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
                            static_cast<cudaStream_t>(stream)>>>(n, a, b, q, mode);

@@ -52,6 +52,10 @@ def test_division_full_range(seed):
     for mode in (0, 1):
         bad = _same(_run(mode, a, b), ref)
         assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
+    nz = b != 0  # the EVD's specialised divisions require a nonzero divisor
+    for mode in (3, 4, 6):
+        bad = _same(_run(mode, a[nz], b[nz]), ref[nz])
+        assert bad.size == 0, (mode, a[nz][bad[:4]], b[nz][bad[:4]])
 
 
 def test_division_near_underflow_and_overflow():
@@ -69,9 +73,26 @@ def test_division_near_underflow_and_overflow():
     for x, y in ((a, b), (a2, b2), (hi, lo), (np.ldexp(np.ones(n), -1074), 1 + rng.random(n))):
         with np.errstate(all="ignore"):
             ref = x / y
-        for mode in (0, 3, 4):
+        for mode in (0, 3, 4, 6):
             bad = _same(_run(mode, x, y), ref)
             assert bad.size == 0, (mode, x[bad[:4]], y[bad[:4]])
+
+
+def test_division_subnormal_ties():
+    # quotients exactly at / next to a midpoint of the subnormal grid:
+    # a = odd * 2^-1074 (or * 2^-1022 ... ) over b = 2, 2(1 +- ulp), 4, 6
+    rng = np.random.default_rng(13)
+    odd = (2 * rng.integers(0, 1 << 51, 1 << 16) + 1).astype(np.float64)
+    xs, ys = [], []
+    for sh in (-1074, -1073, -1060, -1023):
+        for b in (2.0, 2.0 * (1 + 2.0 ** -52), 2.0 * (1 - 2.0 ** -53), 4.0, 6.0, 3.0):
+            xs.append(np.ldexp(odd, sh))
+            ys.append(np.full(odd.size, b))
+    x, y = np.concatenate(xs), np.concatenate(ys)
+    ref = x / y
+    for mode in (0, 3, 4, 6):
+        bad = _same(_run(mode, x, y), ref)
+        assert bad.size == 0, (mode, x[bad[:4]], y[bad[:4]])
 
 
 def test_division_structured_significands():
@@ -92,7 +113,7 @@ def test_division_structured_significands():
     a, b = np.array(A), np.array(B)
     with np.errstate(all="ignore"):
         ref = a / b
-    for mode in (0, 1, 3, 4):
+    for mode in (0, 1, 3, 4, 6):
         bad = _same(_run(mode, a, b), ref)
         assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
 
