@@ -5,12 +5,15 @@ Default workload (N=1): BASELINE.json configs[1], the batched complex 2x2
 Hermitian EVD of r = 2^26 matrices (jsvd_evd2_batched).  One "step" = one
 pass of the EVD over the whole batch with inputs resident in HBM (5.1 GB of
 algorithmic traffic per step, > L2, so no L2 flush is needed).  Multi-GPU: one
-process per GPU (torchrun), every rank runs its own 2^26-matrix shard of a
+process per GPU (torchrun); every rank runs its own 2^26-matrix shard of a
 global batch (counter-based inputs: shard k == slice k of the whole batch) --
 "scaling": "weak", no data-path collective (the batch shards naturally).
 
-Other workloads (--workload): evd_r64 (configs[0]), step_r64 (configs[2]:
-one Jacobi sweep step of the 4096 x 1024 real SVD), batched_c64 (configs[3]).
+Other workloads (--workload, one JSON line each):
+  evd_r64      configs[0]  batched real EVD, r = 2^20 (L2-resident: flushed per step)
+  step_r64     configs[2]  one parallel Jacobi sweep step of the 4096 x 1024 real SVD
+  gesvj_r64    configs[2]  the full SVD (<= 30 sweeps), sweep-steps/s
+  batched_c64  configs[3]  65536 complex 64 x 32 SVDs, SVD/s
 
 --impl reference: the oracle (oracle/, plain C) on this box's host cores, on a
 bounded sample of the same workload per step (this tier's reference arm).
@@ -18,7 +21,6 @@ bounded sample of the same workload per step (this tier's reference arm).
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -29,6 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "2×2 EVDs/s and Jacobi sweep-steps/s; HBM GB/s & % roofline at 1/2/4/8 B200"
+FP64_PEAK_INSTR = 148 * 64 * 1.965e9  # FP64 pipe: 64 lanes/clk/SM x 148 SM x 1965 MHz
 
 
 def load_peaks():
@@ -38,6 +41,14 @@ def load_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic(workload):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
 
 
 # --------------------------------------------------------------- clocks sampler
@@ -92,21 +103,322 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _ncores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
 # --------------------------------------------------------------- workloads
-WORKLOADS = {
-    "evd_c64": dict(cfg=1, desc="BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, "
-                    "r=2^26 per GPU, seed 7", unit="EVD/s", r=1 << 26),
-    "evd_r64": dict(cfg=0, desc="BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, "
-                    "r=2^20 per GPU, seed 42", unit="EVD/s", r=1 << 20),
-}
-EVD_BYTES = {"evd_c64": 32 + 40 + 4 + 1 / 8, "evd_r64": 24 + 32 + 4 + 1 / 8}
+class EvdWorkload:
+    """configs[0] / configs[1]: batched 2x2 EVD (jsvd_evd2_batched)."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        self.name = name
+        self.cplx = name == "evd_c64"
+        self.r = (1 << 26) if self.cplx else (1 << 20)
+        self.unit = "EVD/s"
+        if self.cplx:
+            self.desc = "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 per GPU, seed 7"
+            self.host = synth.evd_cfg2(self.r, off=rank * self.r)
+        else:
+            self.desc = "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 per GPU, seed 42"
+            self.host = synth.evd_cfg1(self.r, off=rank * self.r)
+        self.unit_bytes = (32 + 40 + 4 + 1 / 8) if self.cplx else (24 + 32 + 4 + 1 / 8)
+        self.dev = [torch.from_numpy(a).cuda() for a in self.host]
+        keys = ("lam1", "lam2", "cos", "sin_re") + (("sin_im",) if self.cplx else ())
+        self.out = {k: torch.empty(self.r, dtype=torch.float64, device="cuda") for k in keys}
+        if not self.cplx:
+            self.out["sin_im"] = None
+        self.out["zeta"] = torch.empty(self.r, dtype=torch.int32, device="cuda")
+        self.out["perm"] = torch.empty((self.r + 31) // 32, dtype=torch.int32, device="cuda")
+        # configs[0] is 63 MB (< 126 MB L2): flush L2 between steps (outside the kernel timing)
+        self.flush = None if self.cplx else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.units_per_step = self.r
+        self.kernel = "evd2_vec2_kernel"
+        self.l2_note = ("inputs+outputs %.1f GB per step > 126 MB L2 (no flush needed)"
+                        % (self.unit_bytes * self.r / 1e9)) if self.cplx else \
+            "63 MB working set: a 256 MB buffer is written between timed launches (L2 flush)"
+
+    def prepare(self):
+        if self.flush is not None:
+            self.flush.fill_(1)
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        J.evd2_batched(*self.dev, out=self.out, stream=stream)
+
+    def bytes_per_step(self):
+        return self.unit_bytes * self.r
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hin = [torch.from_numpy(a).pin_memory() for a in self.host]
+        hout = {k: (torch.empty(v.shape, dtype=v.dtype).pin_memory() if v is not None else None)
+                for k, v in self.out.items()}
+
+        def one():
+            for h, d in zip(hin, self.dev):
+                d.copy_(h, non_blocking=True)
+            J.evd2_batched(*self.dev, out=self.out, stream=stream)
+            for k, v in self.out.items():
+                if v is not None:
+                    hout[k].copy_(v, non_blocking=True)
+
+        one()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        h2d = sum(a.nbytes for a in self.host)
+        d2h = sum(v.numel() * v.element_size() for v in self.out.values() if v is not None)
+        return e0.elapsed_time(e1), h2d, d2h
+
+    def cpu_sample(self):
+        """(seconds per call, units per call, description) of the oracle on a sample."""
+        import oracle as O
+        n = min(self.r, 1 << 20)
+        sl = [a[:n] for a in self.host]
+        O.evd2_batched(*[a[:1024] for a in sl])
+        return lambda: O.evd2_batched(*sl), n, f"the first {n} matrices of the batch per call"
 
 
-def make_evd_inputs(name, r, rank):
-    import synth
-    if name == "evd_c64":
-        return synth.evd_cfg2(r, off=rank * r)
-    return synth.evd_cfg1(r, off=rank * r)
+class StepWorkload:
+    """configs[2]: one parallel Jacobi step (jsvd_sweep_step) of the 4096 x 1024
+    real SVD, steps 0.. of the first sweep (every pair transformed), G and V as
+    jsvd_gesvj leaves them after its initial scaling (Eq. skn) and V = I."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        import paper_2202_08361_b200 as J
+        self.name, self.unit = name, "sweep-steps/s"
+        self.desc = ("BASELINE configs[2]: real fp64 one-sided Jacobi SVD 4096x1024, "
+                     "sigma geometric 1->1e-12, one round-robin sweep step (n/2 = 512 pairs)")
+        A, _ = synth.svd_cfg3()
+        self.m, self.n = A.shape
+        k = int(np.floor(np.log2(np.abs(A).max())))
+        s0 = (1022 - int(np.floor(np.log2(self.m)))) - k - 1  # Eq. (skn), as jsvd_gesvj
+        self.A0 = np.ldexp(A, s0)
+        self.G = torch.from_numpy(np.ascontiguousarray(self.A0.T)).cuda().T
+        self.V = torch.eye(self.n, dtype=torch.float64, device="cuda")
+        self.pairs = torch.empty((self.n - 1, self.n), dtype=torch.int32, device="cuda")
+        for s in range(self.n - 1):
+            J.strategy_pairs(self.n, self.n, s, out=self.pairs[s])
+        self.ce = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.cf = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.t = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.mm = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.k = 0
+        self.units_per_step = 1
+        self.kernel = "step_kernel<0,256,1,16>"
+        self.l2_note = "G (32 MB) + V (8 MB) are L2-resident across steps, as in the real iteration"
+
+    def prepare(self):
+        pass
+
+    def reset_counters(self):
+        self.t.zero_()
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        J.sweep_step(self.G, self.V, self.pairs[self.k % (self.n - 1)], col_e=self.ce,
+                     col_f=self.cf, t_dev=self.t, mmax_dev=self.mm, stream=stream)
+        self.k += 1
+
+    def bytes_for(self, steps, transformed):
+        w = 8
+        npairs = self.n // 2
+        skipped = npairs * steps - transformed
+        return transformed * (4 * self.m * w + 4 * self.n * w) + skipped * 2 * self.m * w
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hA = torch.from_numpy(np.ascontiguousarray(self.A0.T)).pin_memory()
+        hG = torch.empty_like(hA).pin_memory()
+        hV = torch.empty((self.n, self.n), dtype=torch.float64).pin_memory()
+        Gt = torch.empty((self.n, self.m), dtype=torch.float64, device="cuda")
+        V = torch.eye(self.n, dtype=torch.float64, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(steps):
+            Gt.copy_(hA, non_blocking=True)
+            J.sweep_step(Gt.T, V, self.pairs[s], col_e=self.ce, col_f=self.cf, t_dev=self.t,
+                         mmax_dev=self.mm, stream=stream)
+            hG.copy_(Gt, non_blocking=True)
+            hV.copy_(V, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hA.numel() * 8, (hG.numel() + hV.numel()) * 8
+
+    def cpu_sample(self):
+        import oracle as O
+        import paper_2202_08361_b200 as J
+        W, c, offs = J.step_rspec(False, self.m)
+        R = O.RSpec.make(W, c, offs)
+        G = np.asfortranarray(self.A0.copy())
+        V = np.asfortranarray(np.eye(self.n))
+        pairs = O.strategy_pairs(self.n, self.n, 0)
+        return lambda: O.step(G, V, pairs, R), 1, "one full step (512 pairs, 4096 x 1024) per call"
+
+
+class BatchedWorkload:
+    """configs[3]: 65536 independent complex 64 x 32 SVDs (jsvd_gesvj_batched),
+    full convergence of every matrix per step."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        self.name, self.unit = name, "SVD/s"
+        self.b, self.m, self.n = 65536, 64, 32
+        self.desc = ("BASELINE configs[3]: batch of 65536 complex fp64 64x32 matrices, "
+                     "re,im ~ N(0,1), full Jacobi SVD (U, Sigma, V) of each, seed 4")
+        self.host = synth.svd_cfg4(self.b, off=rank * self.b)
+        self.A0 = torch.from_numpy(np.ascontiguousarray(np.transpose(self.host, (0, 2, 1)))).cuda()
+        self.A = torch.empty_like(self.A0)
+        self.V = torch.empty((self.b, self.n, self.n), dtype=torch.complex128, device="cuda")
+        self.sig = torch.empty((self.b, self.n), dtype=torch.float64, device="cuda")
+        self.sw = torch.empty(self.b, dtype=torch.int32, device="cuda")
+        self.st = torch.empty(self.b, dtype=torch.int32, device="cuda")
+        self.units_per_step = self.b
+        self.kernel = "batched_svd_kernel<1>"
+        self.l2_note = "2.1 GB of input per step > L2; A restored from a pristine copy before each step (untimed)"
+
+    def prepare(self):
+        self.A.copy_(self.A0)
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        J.gesvj_batched(self.A.transpose(1, 2), V=self.V.transpose(1, 2), sigma=self.sig,
+                        sweeps=self.sw, status=self.st, stream=stream)
+
+    def bytes_per_step(self):
+        w = 16
+        return self.b * (self.m * self.n * w * 2 + self.n * self.n * w + self.n * 8)
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hA = self.A0.cpu().pin_memory()
+        hU = torch.empty_like(hA).pin_memory()
+        hV = torch.empty(self.V.shape, dtype=self.V.dtype).pin_memory()
+        hs = torch.empty(self.sig.shape, dtype=self.sig.dtype).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            self.A.copy_(hA, non_blocking=True)
+            J.gesvj_batched(self.A.transpose(1, 2), V=self.V.transpose(1, 2), sigma=self.sig,
+                            sweeps=self.sw, status=self.st, stream=stream)
+            hU.copy_(self.A, non_blocking=True)
+            hV.copy_(self.V, non_blocking=True)
+            hs.copy_(self.sig, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hA.numel() * 16, (hU.numel() + hV.numel()) * 16 + hs.numel() * 8
+
+    def cpu_sample(self):
+        import oracle as O
+        import paper_2202_08361_b200 as J
+        W, c, offs = J.batched_rspec(True, self.m)
+        R = O.RSpec.make(W, c, offs)
+        k = 256
+        sample = self.host[:k]
+        return lambda: O.gesvj_batched(sample, R), k, f"the first {k} matrices of the batch per call"
+
+
+class GesvjWorkload:
+    """configs[2]: the full SVD (jsvd_gesvj, flat round-robin, <= 30 sweeps) of
+    the 4096 x 1024 real matrix; one bench step = one whole SVD; the unit is
+    the sweep step (n-1 per sweep), so value = sweep-steps/s over the solve."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        import paper_2202_08361_b200 as J
+        self.name, self.unit = name, "sweep-steps/s"
+        self.desc = ("BASELINE configs[2]: real fp64 one-sided Jacobi SVD of one 4096x1024 "
+                     "matrix, sigma geometric 1->1e-12, round-robin, tol sqrt(m) eps, <= 30 sweeps")
+        A, self.sig_true = synth.svd_cfg3()
+        self.m, self.n = A.shape
+        self.host = A
+        self.A0 = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+        self.At = torch.empty_like(self.A0)
+        self.V = torch.empty((self.n, self.n), dtype=torch.float64, device="cuda")
+        self.work = torch.empty(J.gesvj_workspace(False, self.m, self.n), dtype=torch.uint8,
+                                device="cuda")
+        self.units_per_step = None
+        self.kernel = "step_kernel<0,256,1,16>"
+        self.l2_note = "G (32 MB) + V (8 MB) L2-resident; A restored before each solve (untimed)"
+        self.last = None
+
+    def prepare(self):
+        self.At.copy_(self.A0)
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        self.last = J.gesvj(self.At.T, max_sweeps=30, V=self.V.T, work=self.work, stream=stream)
+        self.units_per_step = self.last["sweeps"] * (self.n - 1)
+
+    def bytes_per_step(self):
+        w, T = 8, sum(self.last["tps"])
+        steps = self.last["sweeps"] * (self.n - 1)
+        return (T * (4 * self.m * w + 4 * self.n * w) + (steps * self.n // 2 - T) * 2 * self.m * w)
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hA = self.A0.cpu().pin_memory()
+        hU = torch.empty_like(hA).pin_memory()
+        hV = torch.empty((self.n, self.n), dtype=torch.float64).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            self.At.copy_(hA, non_blocking=True)
+            J.gesvj(self.At.T, max_sweeps=30, V=self.V.T, work=self.work, stream=stream)
+            hU.copy_(self.At, non_blocking=True)
+            hV.copy_(self.V, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hA.numel() * 8, (hU.numel() + hV.numel()) * 8 + self.n * 8
+
+    def cpu_sample(self):
+        import oracle as O
+        import paper_2202_08361_b200 as J
+        W, c, offs = J.step_rspec(False, self.m)
+        R = O.RSpec.make(W, c, offs)
+        s0 = (1022 - int(np.floor(np.log2(self.m)))) - int(np.floor(np.log2(np.abs(self.host).max()))) - 1
+        G = np.asfortranarray(np.ldexp(self.host, s0))
+        V = np.asfortranarray(np.eye(self.n))
+        pairs = O.strategy_pairs(self.n, self.n, 0)
+        return lambda: O.step(G, V, pairs, R), 1, "one full sweep step (512 pairs) per call"
+
+
+WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "step_r64": StepWorkload,
+             "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload}
+
+
+def cpu_baseline(wl, target_s=10.0):
+    """The oracle (never tuned) on this box's host cores, bounded sample."""
+    import oracle as O
+    fn, units, what = wl.cpu_sample()
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        fn()
+        reps += 1
+        if time.perf_counter() - t0 > target_s or reps >= 64:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": units * reps / dt, "unit": wl.unit, "cores": O.num_threads(),
+            "kind": "oracle", "sample": f"{what} x {reps} calls ({dt:.1f} s)"}
 
 
 def run_jsvd(args):
@@ -121,94 +433,101 @@ def run_jsvd(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = WORKLOADS[args.workload]
-    r = wl["r"]
-    cplx = args.workload == "evd_c64"
-    host = make_evd_inputs(args.workload, r, rank)
-    dev = [torch.from_numpy(a).cuda() for a in host]
-    keys = ("lam1", "lam2", "cos", "sin_re") + (("sin_im",) if cplx else ())
-    out = {k: torch.empty(r, dtype=torch.float64, device="cuda") for k in keys}
-    if not cplx:
-        out["sin_im"] = None
-    out["zeta"] = torch.empty(r, dtype=torch.int32, device="cuda")
-    out["perm"] = torch.empty((r + 31) // 32, dtype=torch.int32, device="cuda")
+    wl = WORKLOADS[args.workload](args.workload, rank, world)
     stream = torch.cuda.current_stream()
-
-    def step():
-        J.evd2_batched(*dev, out=out, stream=stream)
+    per_step_events = args.workload in ("evd_r64", "batched_c64", "gesvj_r64")
 
     for _ in range(args.warmup):
-        step()
+        wl.prepare()
+        wl.step(stream)
     torch.cuda.synchronize()
+    if hasattr(wl, "reset_counters"):
+        wl.reset_counters()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     n0 = J.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = []
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        if per_step_events:  # preparation (L2 flush / input restore) outside the timing
+            for _ in range(args.steps):
+                wl.prepare()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                wl.step(stream)
+                b.record(stream)
+                evs.append((a, b))
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                wl.step(stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
     launches = J.launch_count() - n0
-    ms = ev0.elapsed_time(ev1)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
     ms_per_step = ms / args.steps
-    value = world * r * args.steps / (ms / 1e3)
+    value = world * wl.units_per_step * args.steps / (ms / 1e3)
+    if isinstance(wl, GesvjWorkload):
+        extra_g = {"sweeps": wl.last["sweeps"], "status": wl.last["status"],
+                   "transforms_per_sweep": wl.last["tps"]}
 
-    # ---- e2e: the same call with HOST buffers, copies inside the timed region
-    hin = [torch.from_numpy(a).pin_memory() for a in host]
-    hout = {k: (torch.empty(v.shape, dtype=v.dtype).pin_memory() if v is not None else None)
-            for k, v in out.items()}
-    e2e_steps = max(1, min(args.steps, 5))
+    peak, peak_src = load_peaks()
+    extra = {}
+    if isinstance(wl, StepWorkload):
+        transformed = int(wl.t.item())
+        bytes_step = wl.bytes_for(args.steps, transformed) / args.steps
+        extra["transformed_pairs_per_step"] = transformed / args.steps
+    else:
+        bytes_step = wl.bytes_per_step()
+    achieved = bytes_step / (ms_per_step / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.workload),
+                "peak_source": peak_src, "kernel": wl.kernel}
+    if isinstance(wl, GesvjWorkload):
+        extra.update(extra_g)
+        s = wl.last["sigma"].cpu().numpy()
+        extra["sigma_err_normwise"] = float(np.abs(s - wl.sig_true).max() / wl.sig_true[0])
+    if isinstance(wl, BatchedWorkload):
+        sw = wl.sw.float().mean().item()
+        extra["mean_sweeps"] = sw
+        extra["all_converged"] = bool((wl.st == 0).all().item())
+        extra["hbm_roofline_frac"] = achieved / peak
+        # FP64-pipe-bound kernel: report FP64 instruction rate vs the pipe peak
+        # (upper-bound count: every pair of every sweep transformed)
+        m, n = wl.m, wl.n
+        per_pair = (16 * m + 30) + (12 * m + 12 * n + 85)
+        instr = sw * (n - 1) * (n // 2) * per_pair * wl.b
+        ach = instr / (ms_per_step / 1e3)
+        roofline = {"bound": "alu", "achieved": ach / 1e12, "peak": FP64_PEAK_INSTR / 1e12,
+                    "unit": "T FP64-instr/s", "frac": ach / FP64_PEAK_INSTR, "traffic": None,
+                    "peak_source": "derived: 148 SM x 64 FP64 lanes/clk x 1.965 GHz (DESIGN.md)",
+                    "kernel": wl.kernel, "note": "upper-bound op count (all pairs transformed)"}
 
-    def e2e_step():
-        for h, d in zip(hin, dev):
-            d.copy_(h, non_blocking=True)
-        J.evd2_batched(*dev, out=out, stream=stream)
-        for k, v in out.items():
-            if v is not None:
-                hout[k].copy_(v, non_blocking=True)
-
-    e2e_step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
+    e2e_steps = max(1, min(args.steps, 3))
+    ems, h2d, d2h = wl.e2e(stream, e2e_steps)
     if dist:
         t = torch.tensor([ems], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
-    h2d = sum(a.nbytes for a in host)
-    d2h = sum(v.numel() * v.element_size() for v in out.values() if v is not None)
-    e2e_val = world * r * e2e_steps / (ems / 1e3)
-
-    # ---- roofline of the (only) kernel: algorithmic bytes / launch duration
-    peak, peak_src = load_peaks()
-    bytes_per_launch = EVD_BYTES[args.workload] * r
-    achieved = bytes_per_launch / (ms_per_step / 1e3) / 1e9
-    traffic = load_traffic(args.workload)
+    e2e_val = world * wl.units_per_step * e2e_steps / (ems / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.workload, host)
+        cpu = cpu_baseline(wl)
 
     if rank == 0:
         line = {
             "metric": BASELINE_METRIC,
             "value": value,
-            "unit": wl["unit"],
+            "unit": wl.unit,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
@@ -218,58 +537,20 @@ def run_jsvd(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (counter-based SplitMix64, DESIGN.md recipe)",
-            "config": {"workload": wl["desc"], "matrices_per_gpu": r,
-                       "global_batch": world * r, "parallelism": f"batch-shard x{world}",
-                       "l2": "inputs+outputs %.1f GB per step > 126 MB L2 (no flush needed)"
-                             % (bytes_per_launch / 1e9)},
-            "e2e": {"value": e2e_val, "unit": wl["unit"], "h2d_bytes_per_step": h2d,
+            "config": {"workload": wl.desc, "units_per_gpu_step": wl.units_per_step,
+                       "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+                       "l2": wl.l2_note},
+            "e2e": {"value": e2e_val, "unit": wl.unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src, "kernel": "evd2_vec2_kernel",
-                         "bytes_per_unit": EVD_BYTES[args.workload]},
+            "roofline": roofline,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-
-
-def load_traffic(workload):
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        with open(p) as f:
-            return json.load(f).get(workload)
-    except Exception:
-        return None
-
-
-def _ncores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count()
-
-
-def cpu_baseline(workload, host, target_s=10.0):
-    """The oracle (never tuned) on this box's host cores, bounded sample."""
-    import oracle as O
-    r = host[0].size
-    n = min(r, 1 << 22)
-    sl = [a[:n] for a in host]
-    O.evd2_batched(*[a[:1024] for a in sl])  # load + warm
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        O.evd2_batched(*sl)
-        reps += 1
-        if time.perf_counter() - t0 > target_s or reps >= 64:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": n * reps / dt, "unit": "EVD/s", "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"first {n} matrices of the same batch x {reps} passes ({dt:.1f} s)"}
 
 
 def run_reference(args):
@@ -279,39 +560,74 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle as O
-    wl = WORKLOADS[args.workload]
-    per_step = 1 << 20
-    host = make_evd_inputs(args.workload, per_step, 0)
+    wl = ReferenceWorkload(args.workload)
     for _ in range(args.warmup):
-        O.evd2_batched(*host)
+        wl.fn()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.evd2_batched(*host)
+        wl.fn()
     dt = time.perf_counter() - t0
-    v = per_step * args.steps / dt
+    v = wl.units * args.steps / dt
     line = {
-        "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": wl["unit"],
+        "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": wl.unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "matrices_per_step": per_step},
-        "cpu_baseline": {"value": v, "unit": wl["unit"], "cores": O.num_threads(),
-                         "kind": "oracle", "sample": f"{per_step} matrices of the batch per step"},
-        "e2e": {"value": v, "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": wl.desc, "sample_per_step": wl.what},
+        "cpu_baseline": {"value": v, "unit": wl.unit, "cores": O.num_threads(),
+                         "kind": "oracle", "sample": wl.what},
+        "e2e": {"value": v, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+class ReferenceWorkload:
+    """Bounded per-step samples of each workload for the oracle arm (no GPU)."""
+
+    def __init__(self, name):
+        import oracle as O
+        import synth
+        if name in ("evd_c64", "evd_r64"):  # noqa: SIM114
+            n = 1 << 18
+            a = synth.evd_cfg2(n) if name == "evd_c64" else synth.evd_cfg1(n)
+            self.fn = lambda: O.evd2_batched(*a)
+            self.units, self.unit = n, "EVD/s"
+            self.desc = EvdWorkload.__doc__.strip().split("\n")[0] + f" ({name})"
+            self.what = f"{n} matrices of the batch per step"
+        elif name in ("step_r64", "gesvj_r64"):
+            A, _ = synth.svd_cfg3()
+            m, n = A.shape
+            s0 = (1022 - int(np.floor(np.log2(m)))) - int(np.floor(np.log2(np.abs(A).max()))) - 1
+            G = np.asfortranarray(np.ldexp(A, s0))
+            V = np.asfortranarray(np.eye(n))
+            R = O.RSpec.make(256, 1, [16, 8, 4, 2, 1, 128, 64, 32])
+            pairs = O.strategy_pairs(n, n, 0)
+            self.fn = lambda: O.step(G, V, pairs, R)
+            self.units, self.unit = 1, "sweep-steps/s"
+            self.desc = "BASELINE configs[2]: one sweep step of the 4096x1024 real SVD"
+            self.what = "one full step (512 pairs) per step"
+        else:
+            A = synth.svd_cfg4(16)
+            R = O.RSpec.make(32, 1, [16, 8, 4, 2, 1])
+            self.fn = lambda: O.gesvj_batched(A, R)
+            self.units, self.unit = 16, "SVD/s"
+            self.desc = "BASELINE configs[3]: complex 64x32 SVDs"
+            self.what = "16 matrices of the batch per step"
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="jsvd", choices=["jsvd", "reference"])
     ap.add_argument("--workload", default="evd_c64", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = {"evd_c64": 200, "evd_r64": 200, "step_r64": 300, "gesvj_r64": 2,
+                      "batched_c64": 3}[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:
