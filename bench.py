@@ -208,7 +208,7 @@ class StepWorkload:
         s0 = (1022 - int(np.floor(np.log2(self.m)))) - k - 1  # Eq. (skn), as jsvd_gesvj
         self.A0 = np.ldexp(A, s0)
         self.G = torch.from_numpy(np.ascontiguousarray(self.A0.T)).cuda().T
-        self.V = torch.eye(self.n, dtype=torch.float64, device="cuda")
+        self.V = torch.eye(self.n, dtype=torch.float64, device="cuda").T  # column-major view
         self.pairs = torch.empty((self.n - 1, self.n), dtype=torch.int32, device="cuda")
         for s in range(self.n - 1):
             J.strategy_pairs(self.n, self.n, s, out=self.pairs[s])
@@ -246,7 +246,7 @@ class StepWorkload:
         hG = torch.empty_like(hA).pin_memory()
         hV = torch.empty((self.n, self.n), dtype=torch.float64).pin_memory()
         Gt = torch.empty((self.n, self.m), dtype=torch.float64, device="cuda")
-        V = torch.eye(self.n, dtype=torch.float64, device="cuda")
+        V = torch.eye(self.n, dtype=torch.float64, device="cuda").T
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for s in range(steps):
