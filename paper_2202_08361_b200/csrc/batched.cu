@@ -37,7 +37,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <bool CPLX>
+// x 2^-e for a whole column slice, the two-multiply case taken warp-uniformly
+template <int NR, typename E, typename F>
+__device__ __forceinline__ void scaled_loop(const Pow2& f, F&& body) {
+  if (f.two) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) body(j, true);
+  } else {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) body(j, false);
+  }
+}
+
+template <bool CPLX, int NR>
 __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
@@ -49,8 +61,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   PairSlot* slots = reinterpret_cast<PairSlot*>(sV + n * n);
   double* ce = reinterpret_cast<double*>(slots + n / 2);
   double* cf = ce + n;
+  uint8_t* sPairs = reinterpret_cast<uint8_t*>(cf + n);  // (n-1) x n/2 pivot pairs (n <= 64)
   __shared__ unsigned long long sMt, sM0;
-  __shared__ int sT, s_scale, s_sn;
+  __shared__ int sT;
   __shared__ uint64_t wred[kBNW];
 
   const int64_t b = blockIdx.x;
@@ -58,7 +71,14 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int np = static_cast<int>(n / 2);
-  const int NRv = static_cast<int>((m + 31) / 32);
+  const int mi = static_cast<int>(m), ni = static_cast<int>(n);
+  // the flat round-robin ordering (R#20), once per CTA
+  for (int k = threadIdx.x; k < (ni - 1) * np; k += kBT) {
+    int p, q;
+    strategy_pair(ni, ni, k / np, k % np, p, q);
+    sPairs[2 * k] = static_cast<uint8_t>(p);
+    sPairs[2 * k + 1] = static_cast<uint8_t>(q);
+  }
 
   // ---- load A, M0 = max |component| (NaN -> inf), V = I
   uint64_t mx = 0;
@@ -104,7 +124,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   bool converged = false;
   for (C = 0; C < max_sweeps; ++C) {
     if (threadIdx.x == 0) sT = 0;
-    for (int64_t k = 0; k < n - 1; ++k) {
+    for (int k = 0; k < ni - 1; ++k) {
       // ---- line 6: rescale check (every step for flat round-robin)
       {
         const int lm = ilogb_bits(sMt);
@@ -125,34 +145,33 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       }
       // ---- phase A: norms, dot, convergence test (one warp per pair)
       for (int l = warp; l < np; l += kBNW) {
-        int p, q;
-        strategy_pair(n, n, k, l, p, q);
-        const E* gp = sG + static_cast<int64_t>(p) * m;
-        const E* gq = sG + static_cast<int64_t>(q) * m;
+        const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
+        const E* gp = sG + p * mi;
+        const E* gq = sG + q * mi;
+        E xp[NR], xq[NR];
         uint64_t mp = 0, mq = 0;
-        for (int j = 0; j < NRv; ++j) {
-          const int64_t i = static_cast<int64_t>(j) * 32 + lane;
-          if (i < m) {
-            mp = absmax_bits(gp[i], mp);
-            mq = absmax_bits(gq[i], mq);
-          }
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const int i = j * 32 + lane;
+          xp[j] = i < mi ? gp[i] : Elem<CPLX>::zero();
+          xq[j] = i < mi ? gq[i] : Elem<CPLX>::zero();
+          mp = absmax_bits(xp[j], mp);
+          mq = absmax_bits(xq[j], mq);
         }
-        int Ep = __reduce_max_sync(0xffffffffu, ilogb_or_min(mp));
-        int Eq = __reduce_max_sync(0xffffffffu, ilogb_or_min(mq));
+        const int Ep = __reduce_max_sync(0xffffffffu, ilogb_or_min(mp));
+        const int Eq = __reduce_max_sync(0xffffffffu, ilogb_or_min(mq));
         double sp = 0.0, sq = 0.0;
         if (Ep != kIntMin) {
           const Pow2 f(-Ep);
-          for (int j = 0; j < NRv; ++j) {
-            const int64_t i = static_cast<int64_t>(j) * 32 + lane;
-            if (i < m) sp = ssq_acc(f(gp[i]), sp);
-          }
+          scaled_loop<NR, E>(f, [&](int j, bool) {
+            if (j * 32 + lane < mi) sp = ssq_acc(f(xp[j]), sp);
+          });
         }
         if (Eq != kIntMin) {
           const Pow2 f(-Eq);
-          for (int j = 0; j < NRv; ++j) {
-            const int64_t i = static_cast<int64_t>(j) * 32 + lane;
-            if (i < m) sq = ssq_acc(f(gq[i]), sq);
-          }
+          scaled_loop<NR, E>(f, [&](int j, bool) {
+            if (j * 32 + lane < mi) sq = ssq_acc(f(xq[j]), sq);
+          });
         }
         sp = warp_sum<CPLX>(sp);
         sq = warp_sum<CPLX>(sq);
@@ -163,10 +182,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
         if (Ep != kIntMin && Eq != kIntMin) {
           const Pow2 fP(-static_cast<int>(ep)), fQ(-static_cast<int>(eq));
           double ar = 0.0, ai = 0.0;
-          for (int j = 0; j < NRv; ++j) {
-            const int64_t i = static_cast<int64_t>(j) * 32 + lane;
-            if (i < m) dot_acc(fQ(gq[i]), fP(gp[i]), ar, ai);
-          }
+#pragma unroll
+          for (int j = 0; j < NR; ++j)
+            if (j * 32 + lane < mi) dot_acc(fQ(xq[j]), fP(xp[j]), ar, ai);
           ar = warp_sum<CPLX>(ar);
           if (CPLX) ai = warp_sum<CPLX>(ai);
           const Divisor d = make_divisor(fq * fp);
@@ -213,12 +231,11 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       for (int l = warp; l < np; l += kBNW) {
         const PairSlot& sl = slots[l];
         if (!sl.transform) continue;
-        int p, q;
-        strategy_pair(n, n, k, l, p, q);
+        const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
         const double c = sl.c, Cc = sl.C, S = sl.S;
-        E* gp = sG + static_cast<int64_t>(p) * m;
-        E* gq = sG + static_cast<int64_t>(q) * m;
-        for (int64_t i = lane; i < m; i += 32) {
+        E* gp = sG + p * mi;
+        E* gq = sG + q * mi;
+        for (int i = lane; i < mi; i += 32) {
           E a = gp[i], bq = gq[i];
           rot_elem(a, bq, c, Cc, S);
           gp[i] = a;
@@ -226,9 +243,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           Mw = absmax_bits(a, Mw);
           Mw = absmax_bits(bq, Mw);
         }
-        E* vp = sV + static_cast<int64_t>(p) * n;
-        E* vq = sV + static_cast<int64_t>(q) * n;
-        for (int64_t i = lane; i < n; i += 32) {
+        E* vp = sV + p * ni;
+        E* vq = sV + q * ni;
+        for (int i = lane; i < ni; i += 32) {
           E a = vp[i], bq = vq[i];
           rot_elem(a, bq, c, Cc, S);
           vp[i] = a;
@@ -256,9 +273,10 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     double sj = 0.0;
     if (Ej != kIntMin) {
       const Pow2 f(-Ej);
-      for (int jj = 0; jj < NRv; ++jj) {
-        const int64_t i = static_cast<int64_t>(jj) * 32 + lane;
-        if (i < m) sj = ssq_acc(f(g[i]), sj);
+#pragma unroll
+      for (int jj = 0; jj < NR; ++jj) {
+        const int i = jj * 32 + lane;
+        if (i < mi) sj = ssq_acc(f(g[i]), sj);
       }
     }
     sj = warp_sum<CPLX>(sj);
@@ -314,7 +332,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 
 static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
   const size_t w = cplx ? 16 : 8;
-  return w * (m * n + n * n) + sizeof(PairSlot) * (n / 2) + 2 * sizeof(double) * n;
+  return w * (m * n + n * n) + sizeof(PairSlot) * (n / 2) + 2 * sizeof(double) * n +
+         2 * (n - 1) * (n / 2);
 }
 
 static int Fm_host(bool cplx, int64_t m) {
@@ -348,16 +367,20 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
   const int Fm = Fm_host(cplx, m), Kr = cplx ? 1020 : 1022;
   const double tol = std::ldexp(std::sqrt(static_cast<double>(m)), -53);
   cudaError_t e;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(batch), kBT, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
+                                                           sigma, max_sweeps, sweeps_done, status,
+                                                           Fm, Kr, tol);
+  };
   if (cplx) {
-    cudaFuncSetAttribute(batched_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    batched_svd_kernel<true><<<static_cast<unsigned>(batch), kBT, smem, st>>>(
-        m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps, sweeps_done, status, Fm, Kr, tol);
+    if (m <= 32) go(batched_svd_kernel<true, 1>);
+    else if (m <= 64) go(batched_svd_kernel<true, 2>);
+    else go(batched_svd_kernel<true, 4>);
   } else {
-    cudaFuncSetAttribute(batched_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    batched_svd_kernel<false><<<static_cast<unsigned>(batch), kBT, smem, st>>>(
-        m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps, sweeps_done, status, Fm, Kr, tol);
+    if (m <= 32) go(batched_svd_kernel<false, 1>);
+    else if (m <= 64) go(batched_svd_kernel<false, 2>);
+    else go(batched_svd_kernel<false, 4>);
   }
   note_launch();
   e = cudaGetLastError();

@@ -246,29 +246,36 @@ __device__ __forceinline__ void gram(double zr, double zi, double e1, double f1,
 // ---------------------------------------------------------------- strategy
 // R#20: circle method on P players, round r: position 0 = player 0, position
 // k >= 1 = player ((k-1+r) mod (P-1)) + 1; pair i = positions (i, P-1-i).
-__device__ __host__ __forceinline__ int circle_player(int64_t P, int64_t r, int64_t pos) {
-  return pos == 0 ? 0 : static_cast<int>((pos - 1 + r) % (P - 1)) + 1;
+// 0 <= pos, r < P - 1 (or pos = 0), so (pos - 1 + r) mod (P - 1) is one
+// conditional subtraction (n < 2^31: 32-bit arithmetic).
+__device__ __host__ __forceinline__ int circle_player(int P, int r, int pos) {
+  int x = pos - 1 + r;
+  x = x >= P - 1 ? x - (P - 1) : x;
+  return pos == 0 ? 0 : x + 1;
 }
 
 // pair l of step `step` of the block round-robin with B blocks of b = n/B
-__device__ __host__ __forceinline__ void strategy_pair(int64_t n, int64_t B, int64_t step,
-                                                       int64_t l, int& p, int& q) {
-  const int64_t b = n / B;
-  int64_t x, y;
+__device__ __host__ __forceinline__ void strategy_pair(int64_t n64, int64_t B64, int64_t step64,
+                                                       int64_t l64, int& p, int& q) {
+  const int n = static_cast<int>(n64), B = static_cast<int>(B64);
+  const int step = static_cast<int>(step64), l = static_cast<int>(l64);
+  const int b = n / B;
+  int x, y;
   if (step < b - 1) {  // phase I: flat RR inside every block
-    const int64_t beta = l / (b / 2), i = l % (b / 2);
+    const int beta = l / (b / 2), i = l - beta * (b / 2);
     x = beta * b + circle_player(b, step, i);
     y = beta * b + circle_player(b, step, b - 1 - i);
   } else {  // phase II: rounds of flat RR over blocks, b steps per round
-    const int64_t s2 = step - (b - 1), rr = s2 / b, tt = s2 % b;
-    const int64_t i = l / b, j = l % b;
-    const int64_t u = circle_player(B, rr, i), v = circle_player(B, rr, B - 1 - i);
-    const int64_t be = u < v ? u : v, bf = u < v ? v : u;  // block pair (beta < beta')
+    const int s2 = step - (b - 1), rr = s2 / b, tt = s2 - rr * b;
+    const int i = l / b, j = l - i * b;
+    const int u = circle_player(B, rr, i), v = circle_player(B, rr, B - 1 - i);
+    const int be = u < v ? u : v, bf = u < v ? v : u;  // block pair (beta < beta')
+    const int jt = j + tt;
     x = be * b + j;
-    y = bf * b + (j + tt) % b;
+    y = bf * b + (jt >= b ? jt - b : jt);
   }
-  p = static_cast<int>(x < y ? x : y);
-  q = static_cast<int>(x < y ? y : x);
+  p = x < y ? x : y;
+  q = x < y ? y : x;
 }
 
 }  // namespace jsvd
