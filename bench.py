@@ -14,6 +14,7 @@ Other workloads (--workload, one JSON line each):
   step_r64     configs[2]  one parallel Jacobi sweep step of the 4096 x 1024 real SVD
   gesvj_r64    configs[2]  the full SVD (<= 30 sweeps), sweep-steps/s
   batched_c64  configs[3]  65536 complex 64 x 32 SVDs, SVD/s
+  step_c64     configs[4]  one sweep step of the complex 32768 x 8192 SVD (1 GPU)
 
 --impl reference: the oracle (oracle/, plain C) on this box's host cores, on a
 bounded sample of the same workload per step (this tier's reference arm).
@@ -401,8 +402,85 @@ class GesvjWorkload:
         return lambda: O.step(G, V, pairs, R), 1, "one full sweep step (512 pairs) per call"
 
 
+class StepC64Workload(StepWorkload):
+    """configs[4]: one parallel Jacobi step of the complex 32768 x 8192 SVD
+    (4096 pairs, one 8-CTA cluster per pair), block round-robin B = 16 -- the
+    ordering of the column-block-sharded run -- first sweep (all pairs
+    transformed); G (4.3 GB) + V (1.1 GB) far exceed L2."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        import paper_2202_08361_b200 as J
+        self.name, self.unit = name, "sweep-steps/s"
+        self.desc = ("BASELINE configs[4]: complex fp64 Jacobi SVD of one 32768x8192 matrix, "
+                     "sigma log-uniform [1e-8,1], one block-round-robin (B=16) sweep step, 1 GPU")
+        G, _ = synth.svd_cfg5_torch()
+        self.m, self.n = G.shape
+        mx = torch.view_as_real(G).abs().max().item()
+        k = int(np.floor(np.log2(mx)))
+        lg = int(np.floor(np.log2(self.m)))
+        Fm = 1021 - lg - (1 if self.m * self.m >= 2 ** (2 * lg + 1) else 0)
+        s0 = Fm - k - 1  # Eq. (skn), complex
+        torch.view_as_real(G).mul_(2.0 ** s0)
+        self.G = G
+        self.V = torch.eye(self.n, dtype=torch.complex128, device="cuda").T
+        self.B = 16
+        self.pairs = torch.empty((self.n - 1, self.n), dtype=torch.int32, device="cuda")
+        for s in range(self.n - 1):
+            J.strategy_pairs(self.n, self.B, s, out=self.pairs[s])
+        self.ce = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.cf = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.t = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.mm = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.k = 0
+        self.units_per_step = 1
+        self.kernel = "step_kernel<1,512,8,8>"
+        self.l2_note = "G 4.3 GB + V 1.1 GB >> L2"
+
+    def bytes_for(self, steps, transformed):
+        w = 16
+        npairs = self.n // 2
+        skipped = npairs * steps - transformed
+        return transformed * (4 * self.m * w + 4 * self.n * w) + skipped * 2 * self.m * w
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hG = torch.empty((self.n, self.m), dtype=torch.complex128).pin_memory()
+        hG.copy_(self.G.T)
+        hV = torch.empty((self.n, self.n), dtype=torch.complex128).pin_memory()
+        Gt = torch.empty((self.n, self.m), dtype=torch.complex128, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(steps):
+            Gt.copy_(hG, non_blocking=True)
+            J.sweep_step(Gt.T, self.V, self.pairs[s], col_e=self.ce, col_f=self.cf, t_dev=self.t,
+                         mmax_dev=self.mm, stream=stream)
+            hG.copy_(Gt, non_blocking=True)
+            hV.copy_(self.V.T, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hG.numel() * 16, (hG.numel() + hV.numel()) * 16
+
+    def cpu_sample(self):
+        import oracle as O
+        import paper_2202_08361_b200 as J
+        W, c, offs = J.step_rspec(True, self.m)
+        R = O.RSpec.make(W, c, offs)
+        npairs = 16  # a bounded sample: 16 of the 4096 pairs of a step
+        cols = self.pairs[0][: 2 * npairs].cpu().numpy()
+        G = np.asfortranarray(self.G[:, cols.tolist()].cpu().numpy())
+        V = np.asfortranarray(np.eye(2 * npairs, dtype=np.complex128))
+        pairs = np.arange(2 * npairs, dtype=np.int32).reshape(-1, 2)
+        frac = npairs / (self.n // 2)
+        return (lambda: O.step(G, V, pairs, R)), frac, \
+            f"{npairs} of the {self.n // 2} pairs of a step per call (units = fraction of a step)"
+
+
 WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "step_r64": StepWorkload,
-             "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload}
+             "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload,
+             "step_c64": StepC64Workload}
 
 
 def cpu_baseline(wl, target_s=10.0):
@@ -481,7 +559,7 @@ def run_jsvd(args):
 
     peak, peak_src = load_peaks()
     extra = {}
-    if isinstance(wl, StepWorkload):
+    if isinstance(wl, StepWorkload):  # (StepC64Workload included)
         transformed = int(wl.t.item())
         bytes_step = wl.bytes_for(args.steps, transformed) / args.steps
         extra["transformed_pairs_per_step"] = transformed / args.steps
@@ -627,7 +705,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         args.steps = {"evd_c64": 200, "evd_r64": 200, "step_r64": 300, "gesvj_r64": 2,
-                      "batched_c64": 3}[args.workload]
+                      "batched_c64": 3, "step_c64": 50}[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -110,6 +110,27 @@ def svd_cfg5(m=32768, n=8192, seed=SEEDS[5], log_range=8.0):
     return np.asfortranarray((q1 * sig) @ q2.conj().T), sig
 
 
+def svd_cfg5_torch(m=32768, n=8192, seed=SEEDS[5], log_range=8.0, device="cuda"):
+    """configs[4] generated on the GPU with torch (QR + GEMM would take hours in
+    numpy): A = Q1 diag(sigma) Q2^H, Q from torch.linalg.qr of complex Gaussian
+    matrices drawn by this module's counter-based generator; sigma = 10^{-8 u}.
+    Returns (A as an (m, n) column-major complex128 CUDA tensor, sigma numpy)."""
+    import torch
+    sig = 10.0 ** (-log_range * uniform(n, seed, 9))
+
+    def cgauss(r, c, stream):
+        re = torch.from_numpy(gauss(r * c, seed, stream)).to(device)
+        im = torch.from_numpy(gauss(r * c, seed, stream + 1)).to(device)
+        return torch.complex(re, im).reshape(c, r).T  # column-major (r, c) view
+
+    q1, _ = torch.linalg.qr(cgauss(m, n, 0))
+    q2, _ = torch.linalg.qr(cgauss(n, n, 2))
+    A = (q1 * torch.from_numpy(sig).to(device)) @ q2.conj().T
+    At = A.T.contiguous()  # (n, m) row-major == (m, n) column-major
+    del q1, q2, A
+    return At.T, sig
+
+
 def svd_cfg4(batch, m=64, n=32, seed=SEEDS[4], off=0):
     """(batch, m, n) complex128; entries re, im ~ N(0,1) i.i.d. (configs[3]).
     Matrix b's column-major (re, im) stream starts at global element b*m*n."""
