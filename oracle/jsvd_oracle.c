@@ -354,12 +354,15 @@ double orc_rot(int cplx, int64_t l, double *xp, double *xq, double c, double C, 
 
 /* One step of Alg 4.1 lines 7-38 over explicit disjoint pairs,
  * s = 1 (R#13), P = I (R#20).  col_e/col_f receive the norms of the step's
- * columns BEFORE rotation; *t += transformed pairs; *mmax = max(*mmax, M).   */
-int orc_step(int cplx, int64_t m, int64_t n, double *G, int64_t ldg, double *V, int64_t ldv,
+ * columns BEFORE rotation; *t += transformed pairs; *mmax = max(*mmax, M).
+ * V has nv rows (the order of V; Alg 3.4 with l = n) and the same
+ * column indexing as G -- nv > n when the caller holds only some columns.    */
+int orc_step(int cplx, int64_t m, int64_t n, int64_t nv, double *G, int64_t ldg, double *V,
+             int64_t ldv,
              const int32_t *pairs, int64_t npairs, double tol, const orc_rspec *R,
              double *col_e, double *col_f, int64_t *t_out, double *mmax)
 {
-  if (!rspec_ok(R) || m < 1 || n < 2 || ldg < m || (V && ldv < n)) return ORC_EINVAL;
+  if (!rspec_ok(R) || m < 1 || n < 2 || ldg < m || (V && (nv < n || ldv < nv))) return ORC_EINVAL;
   const int64_t w = cplx ? 2 : 1;
   double upsilon = tol > 0.0 ? tol : orc_upsilon(m);
   int64_t t = 0;
@@ -386,7 +389,7 @@ int orc_step(int cplx, int64_t m, int64_t n, double *G, int64_t ldg, double *V, 
     orc_evd2_one(cplx, b11, b22, br, bi, ORC_EVD_TAN | ORC_EVD_NOBACKSCALE, &l1, &l2, &c, &C, &S,
                  &z, &pp); /* diamond */
     double Mp = orc_rot(cplx, m, gp, gq, c, C, S); /* star: G */
-    if (V) orc_rot(cplx, n, V + w * p * ldv, V + w * q * ldv, c, C, S); /* star: V */
+    if (V) orc_rot(cplx, nv, V + w * p * ldv, V + w * q * ldv, c, C, S); /* star: V */
     if (Mp > M) M = Mp;
     t += 1;
   }
@@ -530,7 +533,7 @@ int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V,
       orc_strategy_pairs(n, B, k, pairs);
       int64_t t = 0;
       double M = 0.0;
-      orc_step(cplx, m, n, A, lda, V, ldv, pairs, n / 2, upsilon, R, ce, cf, &t, &M);
+      orc_step(cplx, m, n, n, A, lda, V, ldv, pairs, n / 2, upsilon, R, ce, cf, &t, &M);
       T += t;
       Mt = fmax(Mt, M); /* line 38 */
     }

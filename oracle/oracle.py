@@ -74,7 +74,7 @@ def lib():
         L.orc_rot.restype = _D
         L.orc_rot.argtypes = [ct.c_int, _I64, ct.c_void_p, ct.c_void_p, _D, _D, _D]
         L.orc_step.restype = ct.c_int
-        L.orc_step.argtypes = [ct.c_int, _I64, _I64, ct.c_void_p, _I64, ct.c_void_p, _I64,
+        L.orc_step.argtypes = [ct.c_int, _I64, _I64, _I64, ct.c_void_p, _I64, ct.c_void_p, _I64,
                                ct.c_void_p, _I64, _D, ct.POINTER(RSpec), ct.c_void_p,
                                ct.c_void_p, ct.POINTER(_I64), _PD]
         L.orc_strategy_pairs.restype = ct.c_int
@@ -201,16 +201,17 @@ def _mat_view(A):
 
 
 def step(G, V, pairs, R, tol=0.0):
-    """One step in place on Fortran-ordered G (m x n) and V (n x n)."""
+    """One step in place on Fortran-ordered G (m x ncols) and V (nv x ncols)."""
     cplx, gb, ldg = _mat_view(G)
     _, vb, ldv = _mat_view(V) if V is not None else (cplx, None, G.shape[1])
     m, n = G.shape
+    nv = V.shape[0] if V is not None else n
     pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1)
     ce = np.zeros(n, np.float64)
     cf = np.zeros(n, np.float64)
     t = _I64(0)
     M = _D(0.0)
-    st = lib().orc_step(cplx, m, n, _ptr(gb), ldg, _ptr(vb), ldv, _ptr(pairs), pairs.size // 2,
+    st = lib().orc_step(cplx, m, n, nv, _ptr(gb), ldg, _ptr(vb), ldv, _ptr(pairs), pairs.size // 2,
                         tol, ct.byref(R), _ptr(ce), _ptr(cf), ct.byref(t), ct.byref(M))
     if st != OK:
         raise ValueError(f"orc_step status {st}")

@@ -67,6 +67,14 @@ def lib():
         L.jsvd_gesvj_batched.restype = ct.c_int
         L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
                                          _i64, _vp, _i32, _vp, _vp, _vp]
+        L.jsvd_maxnorm.restype = ct.c_int
+        L.jsvd_maxnorm.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp]
+        L.jsvd_scale.restype = ct.c_int
+        L.jsvd_scale.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _i32, _vp]
+        L.jsvd_colnorms.restype = ct.c_int
+        L.jsvd_colnorms.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp]
+        L.jsvd_normalize.restype = ct.c_int
+        L.jsvd_normalize.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp]
         L.jsvd_status_string.restype = ct.c_char_p
         L.jsvd_status_string.argtypes = [ct.c_int]
         L.jsvd_launch_count.restype = _i64
@@ -175,14 +183,17 @@ def _mat(t, name):
 
 def sweep_step(G, V, pairs, tol=0.0, col_e=None, col_f=None, t_dev=None, mmax_dev=None,
                stream=None):
-    """One Jacobi step in place on column-major G (m x n) and V (n x n)."""
+    """One Jacobi step in place on column-major G (m x ncols) and V (n x ncols):
+    V has as many columns as G (the columns a driver holds) and n rows (the
+    order of the full V; n = ncols for an unsharded SVD)."""
     cplx, ldg = _mat(G, "G")
     m, n = G.shape
     ldv = n
     if V is not None:
         cv, ldv = _mat(V, "V")
-        if cv != cplx or V.shape != (n, n):
-            raise ValueError("V must be n x n of G's dtype")
+        if cv != cplx or V.shape[1] != n or V.shape[0] < n:
+            raise ValueError("V must be (n >= ncols) x ncols of G's dtype")
+        n = V.shape[0]
     dev = G.device
     col_e = torch.empty(n, dtype=torch.float64, device=dev) if col_e is None else col_e
     col_f = torch.empty(n, dtype=torch.float64, device=dev) if col_f is None else col_f
@@ -196,6 +207,45 @@ def sweep_step(G, V, pairs, tol=0.0, col_e=None, col_f=None, t_dev=None, mmax_de
                                _p(mmax_dev), _stream(stream))
     _check(st, "jsvd_sweep_step")
     return dict(col_e=col_e, col_f=col_f, t=t_dev, mmax=mmax_dev)
+
+
+def maxnorm(G, out=None, stream=None):
+    """max |component| of column-major G into the device scalar `out` (max-reduced)."""
+    cplx, ld = _mat(G, "G")
+    m, n = G.shape
+    out = torch.zeros(1, dtype=torch.float64, device=G.device) if out is None else out
+    _check(lib().jsvd_maxnorm(C64 if cplx else R64, m, n, _p(G), ld, _p(out), _stream(stream)),
+           "jsvd_maxnorm")
+    return out
+
+
+def scale(G, s, stream=None):
+    """G <- 2^s G in place (one rounding per component)."""
+    cplx, ld = _mat(G, "G")
+    m, n = G.shape
+    _check(lib().jsvd_scale(C64 if cplx else R64, m, n, _p(G), ld, int(s), _stream(stream)),
+           "jsvd_scale")
+    return G
+
+
+def colnorms(G, col_e=None, col_f=None, stream=None):
+    """(e, f) of every column of G, in the step kernel's reduction order."""
+    cplx, ld = _mat(G, "G")
+    m, n = G.shape
+    col_e = torch.empty(n, dtype=torch.float64, device=G.device) if col_e is None else col_e
+    col_f = torch.empty(n, dtype=torch.float64, device=G.device) if col_f is None else col_f
+    _check(lib().jsvd_colnorms(C64 if cplx else R64, m, n, _p(G), ld, _p(col_e), _p(col_f),
+                               _stream(stream)), "jsvd_colnorms")
+    return col_e, col_f
+
+
+def normalize(G, col_e, col_f, stream=None):
+    """u_j = 2^-e_j g_j / f_j in place."""
+    cplx, ld = _mat(G, "G")
+    m, n = G.shape
+    _check(lib().jsvd_normalize(C64 if cplx else R64, m, n, _p(G), ld, _p(col_e), _p(col_f),
+                                _stream(stream)), "jsvd_normalize")
+    return G
 
 
 def gesvj_workspace(cplx, m, n):
