@@ -478,9 +478,86 @@ class StepC64Workload(StepWorkload):
             f"{npairs} of the {self.n // 2} pairs of a step per call (units = fraction of a step)"
 
 
+class DistC64Workload:
+    """configs[4] column-block sharded over the torchrun ranks (N = 1, 2, 4, 8):
+    paper_2202_08361_b200.dist with NCCL send/recv block exchange; one bench
+    step = one global sweep step (4096 pairs over all ranks); the timed window
+    straddles the first phase-II round's block exchange."""
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        from paper_2202_08361_b200.dist import (BlockSchedule, CudaCompute, DistJacobi,
+                                                LocalRanks, TorchDistRanks, scatter_columns)
+        self.name, self.unit = name, "sweep-steps/s"
+        self.desc = ("BASELINE configs[4]: complex fp64 Jacobi SVD of one 32768x8192 matrix, "
+                     f"column blocks (B=16) sharded over {world} GPU(s), NCCL block exchange")
+        A, _ = synth.svd_cfg5_torch()
+        self.m, self.n = A.shape
+        self.S = BlockSchedule(self.n, 16, world)
+        cols = torch.from_numpy(scatter_columns(None, self.S, rank)).cuda()
+        Gt = A.T[cols].contiguous()  # (ncols_local, m)
+        del A
+        torch.cuda.empty_cache()
+        ranks = TorchDistRanks() if world > 1 else LocalRanks(1)
+        self.D = DistJacobi([Gt], self.S, ranks, CudaCompute(), cplx=True)
+        self.D.begin_sweep()
+        self.k = 0
+        self.world = world
+        self.units_per_step = 1.0 / world  # value = world * units * steps / time = global steps/s
+        self.kernel = "step_kernel<1,512,8,8>"
+        self.l2_note = "local G + V >> L2"
+
+    def prepare(self):
+        pass
+
+    def skip_to(self, k0):
+        while self.k < k0:
+            self.step(None)
+
+    def reset_counters(self):
+        pass
+
+    def step(self, stream):
+        self.D.step(self.k)
+        self.k += 1
+
+    def bytes_for(self, steps, transformed):
+        w = 16
+        return transformed * (4 * self.m * w + 4 * self.n * w)
+
+    def e2e(self, stream, steps):
+        """local blocks in from pinned host memory, `steps` steps, local G and V back out."""
+        import torch
+        Gt, Vt = self.D.Gts[0], self.D.Vts[0]
+        hG = Gt.cpu().pin_memory()
+        hV = torch.empty(Vt.shape, dtype=Vt.dtype).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        self.D.Gts[0].copy_(hG, non_blocking=True)
+        for _ in range(steps):
+            self.step(stream)
+        hG.copy_(self.D.Gts[0], non_blocking=True)
+        hV.copy_(self.D.Vts[0], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hG.numel() * 16, (hG.numel() + hV.numel()) * 16
+
+    def cpu_sample(self):
+        import oracle as O
+        import paper_2202_08361_b200 as J
+        R = O.RSpec.make(*J.step_rspec(True, self.m))
+        npairs = 16
+        G = np.asfortranarray(self.D.Gts[0][: 2 * npairs].cpu().numpy().T)
+        V = np.asfortranarray(np.eye(2 * npairs, dtype=np.complex128))
+        pairs = np.arange(2 * npairs, dtype=np.int32).reshape(-1, 2)
+        return (lambda: O.step(G, V, pairs, R)), npairs / (self.n // 2), \
+            f"{npairs} of the {self.n // 2} pairs of a step per call (units = fraction of a step)"
+
+
 WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "step_r64": StepWorkload,
              "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload,
-             "step_c64": StepC64Workload}
+             "step_c64": StepC64Workload, "dist_c64": DistC64Workload}
 
 
 def cpu_baseline(wl, target_s=10.0):
@@ -521,6 +598,9 @@ def run_jsvd(args):
     torch.cuda.synchronize()
     if hasattr(wl, "reset_counters"):
         wl.reset_counters()
+    if hasattr(wl, "skip_to"):  # dist: let the timed window straddle a block exchange
+        wl.skip_to(max(wl.k, 2 * wl.S.b - 1 - args.steps // 2))
+        torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -563,6 +643,10 @@ def run_jsvd(args):
         transformed = int(wl.t.item())
         bytes_step = wl.bytes_for(args.steps, transformed) / args.steps
         extra["transformed_pairs_per_step"] = transformed / args.steps
+    elif isinstance(wl, DistC64Workload):  # per-GPU share; first sweep: every pair transforms
+        bytes_step = wl.bytes_for(1, wl.n // 2) / world
+        extra.update(scaling_note="strong: one SVD, columns sharded", first_step_timed=wl.k - args.steps,
+                     exchange_after_step=2 * wl.S.b - 2)
     else:
         bytes_step = wl.bytes_per_step()
     achieved = bytes_step / (ms_per_step / 1e3) / 1e9
@@ -705,7 +789,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         args.steps = {"evd_c64": 200, "evd_r64": 200, "step_r64": 300, "gesvj_r64": 2,
-                      "batched_c64": 3, "step_c64": 50}[args.workload]
+                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100}[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:

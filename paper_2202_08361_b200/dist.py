@@ -31,7 +31,7 @@ import math
 import numpy as np
 import torch
 
-__all__ = ["BlockSchedule", "LocalRanks", "TorchDistRanks", "CudaCompute", "gesvj_dist",
+__all__ = ["BlockSchedule", "LocalRanks", "TorchDistRanks", "CudaCompute", "DistJacobi", "gesvj_dist",
            "scatter_columns", "gather_columns", "Fm", "Kr"]
 
 
@@ -258,94 +258,120 @@ def gather_columns(parts, sched):
     return out
 
 
-def gesvj_dist(Gts, sched, ranks, compute, max_sweeps=30, cplx=False):
-    """Run Alg 4.1 on column blocks.
+class DistJacobi:
+    """Alg 4.1 on column blocks, step by step (gesvj_dist drives it to the end;
+    bench.py times its steps).
 
-    Gts: list (one per local rank of `ranks`) of Gt tensors (ncols_local, m) holding
-    the round-0 column blocks (see scatter_columns).  On exit Gts hold U's columns
-    (same layout), and the returned dict has Vts (local V columns, layout as Gts),
-    the globally sorted sigma / sigma_e / sigma_f, the permutation `perm`
-    (global column index of each sorted singular value), sweeps, tps, status.
+    Gts: list (one per local rank of `ranks`) of Gt tensors (ncols_local, m)
+    holding the round-0 column blocks (see scatter_columns).
     """
-    nl = len(ranks.ranks)
-    m = Gts[0].shape[1]
-    n, b = sched.n, sched.b
-    like = Gts[0]
-    # ---- line 1: M0 (global), s0, G1 = 2^s0 G
-    Mt = [compute.scalar(0.0, like) for _ in range(nl)]
-    for G, M in zip(Gts, Mt):
-        compute.maxnorm(G, M)
-    ranks.allreduce_max(Mt)
-    M0 = float(Mt[0].item())
-    if math.isinf(M0) or math.isnan(M0):
-        raise ValueError("non-finite input (P:1112)")
-    if M0 == 0.0:
-        raise ValueError("zero matrix (P:1114)")
-    F, K = Fm(cplx, m), Kr(cplx)
-    s = F - _ilogb(M0) - 1
-    for G in Gts:
-        compute.scale(G, s)
-    for M in Mt:
-        M.fill_(math.ldexp(M0, s))
-    # ---- line 2: V = I (local columns)
-    Vts = []
-    for rank, G in zip(ranks.ranks, Gts):
-        cols = scatter_columns(None, sched, rank)
-        V = torch.zeros((len(cols), n), dtype=G.dtype, device=G.device)
-        V[torch.arange(len(cols)), torch.from_numpy(cols).to(G.device)] = 1.0
-        Vts.append(V)
-    Gb = [torch.empty_like(G) for G in Gts]
-    Vb = [torch.empty_like(V) for V in Vts]
-    tdev = [compute.counter(like) for _ in range(nl)]
-    ce = [torch.empty(G.shape[0], dtype=torch.float64, device=G.device) for G in Gts]
-    cf = [torch.empty(G.shape[0], dtype=torch.float64, device=G.device) for G in Gts]
-    moves = sched.moves()
-    tps, converged, C = [], False, 0
-    for C in range(max_sweeps):
-        for t in tdev:
+
+    def __init__(self, Gts, sched, ranks, compute, cplx=False):
+        self.sched, self.ranks, self.compute, self.cplx = sched, ranks, compute, cplx
+        nl = len(ranks.ranks)
+        self.m = Gts[0].shape[1]
+        like = Gts[0]
+        # ---- line 1: M0 (global), s0, G1 = 2^s0 G
+        self.Mt = [compute.scalar(0.0, like) for _ in range(nl)]
+        for G, M in zip(Gts, self.Mt):
+            compute.maxnorm(G, M)
+        ranks.allreduce_max(self.Mt)
+        M0 = float(self.Mt[0].item())
+        if math.isinf(M0) or math.isnan(M0):
+            raise ValueError("non-finite input (P:1112)")
+        if M0 == 0.0:
+            raise ValueError("zero matrix (P:1114)")
+        self.F, self.K = Fm(cplx, self.m), Kr(cplx)
+        self.s = self.F - _ilogb(M0) - 1
+        for G in Gts:
+            compute.scale(G, self.s)
+        for M in self.Mt:
+            M.fill_(math.ldexp(M0, self.s))
+        # ---- line 2: V = I (local columns)
+        self.Gts, self.Vts = Gts, []
+        for rank, G in zip(ranks.ranks, Gts):
+            cols = scatter_columns(None, sched, rank)
+            V = torch.zeros((len(cols), sched.n), dtype=G.dtype, device=G.device)
+            V[torch.arange(len(cols)), torch.from_numpy(cols).to(G.device)] = 1.0
+            self.Vts.append(V)
+        self.Gb = [torch.empty_like(G) for G in Gts]
+        self.Vb = [torch.empty_like(V) for V in self.Vts]
+        self.tdev = [compute.counter(like) for _ in range(nl)]
+        self.ce = [torch.empty(G.shape[0], dtype=torch.float64, device=G.device) for G in Gts]
+        self.cf = [torch.empty(G.shape[0], dtype=torch.float64, device=G.device) for G in Gts]
+        self.moves = sched.moves()
+
+    def begin_sweep(self):
+        for t in self.tdev:
             t.zero_()
-        for k in range(n - 1):
-            if sched.is_checkpoint(k):  # Eq. (skr) on the global M-tilde (R#21)
-                ranks.allreduce_max(Mt)
-                mt = float(Mt[0].item())
-                lm = _ilogb(mt)
-                if K - lm < 0:
-                    sn = F - lm - 1
-                    for G in Gts:
-                        compute.scale(G, sn)
-                    for M in Mt:
-                        M.fill_(math.ldexp(mt, sn))
-                    s += sn
-            for rank, G, V, t, M, e, f in zip(ranks.ranks, Gts, Vts, tdev, Mt, ce, cf):
-                compute.step(G, V, sched.local_pairs(rank, k), (rank, k), t, M, e, f)
-            if k >= b - 1 and (k - (b - 1)) % b == b - 1:  # end of a phase-II round
-                ranks.exchange(moves, [Gts, Vts], [Gb, Vb], b)
-                Gts, Gb = Gb, Gts
-                Vts, Vb = Vb, Vts
-        ranks.allreduce_sum(tdev)
-        T = int(tdev[0].item())
+
+    def step(self, k):
+        """Step k in [0, n-1) of the current sweep, incl. its check point and,
+        at the end of a phase-II round, the block exchange."""
+        S, b = self.sched, self.sched.b
+        if S.is_checkpoint(k):  # Eq. (skr) on the global M-tilde (R#21)
+            self.ranks.allreduce_max(self.Mt)
+            mt = float(self.Mt[0].item())
+            lm = _ilogb(mt)
+            if self.K - lm < 0:
+                sn = self.F - lm - 1
+                for G in self.Gts:
+                    self.compute.scale(G, sn)
+                for M in self.Mt:
+                    M.fill_(math.ldexp(mt, sn))
+                self.s += sn
+        for rank, G, V, t, M, e, f in zip(self.ranks.ranks, self.Gts, self.Vts, self.tdev,
+                                          self.Mt, self.ce, self.cf):
+            self.compute.step(G, V, S.local_pairs(rank, k), (rank, k), t, M, e, f)
+        if k >= b - 1 and (k - (b - 1)) % b == b - 1:  # end of a phase-II round
+            self.ranks.exchange(self.moves, [self.Gts, self.Vts], [self.Gb, self.Vb], b)
+            self.Gts, self.Gb = self.Gb, self.Gts
+            self.Vts, self.Vb = self.Vb, self.Vts
+
+    def end_sweep(self):
+        self.ranks.allreduce_sum(self.tdev)
+        return int(self.tdev[0].item())
+
+    def finalize(self):
+        """P:1473-1485 (R#23, R#24): local norms, normalise, global sort."""
+        S, n = self.sched, self.sched.n
+        keys = []
+        for rank, G in zip(self.ranks.ranks, self.Gts):
+            e, f = self.compute.colnorms(G)
+            self.compute.normalize(G, e, f)
+            gcol = torch.from_numpy(scatter_columns(None, S, rank)).to(torch.float64).to(e.device)
+            keys.append(torch.stack([e, f, gcol], 1))
+        allk = self.ranks.allgather_cat(keys)[0].cpu().numpy()
+        e_all = np.where(np.isinf(allk[:, 0]), allk[:, 0], allk[:, 0] - self.s)
+        order = sorted(range(n), key=lambda j: (-e_all[j], -allk[j, 1], allk[j, 2]))
+        sig_e = e_all[order]
+        sig_f = allk[order, 1]
+        sigma = np.array([0.0 if math.isinf(e) else math.ldexp(f, int(max(min(e, 1e5), -1e5)))
+                          for e, f in zip(sig_e, sig_f)])
+        perm = allk[order, 2].astype(np.int64)
+        return dict(Gts=self.Gts, Vts=self.Vts, sigma=sigma, sigma_e=sig_e, sigma_f=sig_f,
+                    perm=perm)
+
+
+def gesvj_dist(Gts, sched, ranks, compute, max_sweeps=30, cplx=False):
+    """Run Alg 4.1 on column blocks to convergence.
+
+    On exit the returned dict has Gts (U's columns, same layout as the input),
+    Vts (local V columns), the globally sorted sigma / sigma_e / sigma_f, the
+    permutation `perm` (global column index of each sorted singular value),
+    sweeps, tps (T per sweep) and status (0, or 1 = ENOCONV).
+    """
+    D = DistJacobi(Gts, sched, ranks, compute, cplx)
+    tps, converged, C = [], False, max_sweeps
+    for c in range(max_sweeps):
+        D.begin_sweep()
+        for k in range(sched.n - 1):
+            D.step(k)
+        T = D.end_sweep()
         tps.append(T)
         if T == 0:
-            converged = True
-            C += 1
+            converged, C = True, c + 1
             break
-    else:
-        C = max_sweeps
-    # ---- finalize (P:1473-1485; R#23, R#24): local norms, normalise, global sort
-    keys = []
-    for rank, G in zip(ranks.ranks, Gts):
-        e, f = compute.colnorms(G)
-        compute.normalize(G, e, f)
-        gcol = torch.from_numpy(scatter_columns(None, sched, rank)).to(torch.float64).to(e.device)
-        keys.append(torch.stack([e, f, gcol], 1))
-    allk = ranks.allgather_cat(keys)[0].cpu().numpy()
-    e_all = np.where(np.isinf(allk[:, 0]), allk[:, 0], allk[:, 0] - s)
-    order = sorted(range(n), key=lambda j: (-e_all[j], -allk[j, 1], allk[j, 2]))
-    sig_e = e_all[order]
-    sig_f = allk[order, 1]
-    sigma = np.array([0.0 if math.isinf(e) else math.ldexp(f, int(max(min(e, 1e5), -1e5)))
-                      for e, f in zip(sig_e, sig_f)])
-    perm = allk[order, 2].astype(np.int64)
-    # write the (possibly swapped) buffers back into the caller's list objects
-    return dict(Gts=Gts, Vts=Vts, sigma=sigma, sigma_e=sig_e, sigma_f=sig_f, perm=perm,
-                sweeps=C, tps=tps, status=0 if converged else 1)
+    out = D.finalize()
+    out.update(sweeps=C, tps=tps, status=0 if converged else 1)
+    return out
