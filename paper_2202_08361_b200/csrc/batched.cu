@@ -208,17 +208,19 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       if (warp == 0) {
         int tcount = 0;
         for (int l = lane; l < np + (32 - (np % 32)) % 32; l += 32) {
-          bool tr = false;
-          if (l < np) {
-            PairSlot& sl = slots[l];
-            tr = sl.transform;
+          // every lane runs (dummy pair past np / for converged pairs) so the
+          // EVD's rare-case votes use the full warp mask
+          const bool tr = l < np && slots[l].transform;
+          if (__any_sync(kFull, tr)) {
+            const PairSlot& s0 = slots[l < np ? l : 0];
+            double b11, b22, br, bi;
+            gram(tr ? s0.zr : 0.0, tr ? s0.zi : 0.0, tr ? s0.ep : 0.0, tr ? s0.fp : 1.0,
+                 tr ? s0.eq : 0.0, tr ? s0.fq : 1.0, b11, b22, br, bi);
+            const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi, kFull);
             if (tr) {
-              double b11, b22, br, bi;
-              gram(sl.zr, sl.zi, sl.ep, sl.fp, sl.eq, sl.fq, b11, b22, br, bi);
-              const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi);
-              sl.c = o.c;
-              sl.C = o.sr;
-              sl.S = o.si;
+              slots[l].c = o.c;
+              slots[l].C = o.sr;
+              slots[l].S = o.si;
             }
           }
           tcount += __popc(__ballot_sync(0xffffffffu, tr));

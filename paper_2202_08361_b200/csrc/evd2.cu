@@ -30,32 +30,37 @@ __global__ void __launch_bounds__(256) evd2_vec2_kernel(
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t l0 = 2 * tid;
-  bool p0 = false, p1 = false;
+  // every lane runs the EVD (zeros past the tail) so the rare-case votes can
+  // use the full warp mask
+  double2 x11 = make_double2(0.0, 0.0), x22 = x11, xre = x11, xim = x11;
   if (l0 + 1 < r) {
-    const double2 x11 = __ldcs(reinterpret_cast<const double2*>(a11) + tid);
-    const double2 x22 = __ldcs(reinterpret_cast<const double2*>(a22) + tid);
-    const double2 xre = __ldcs(reinterpret_cast<const double2*>(are) + tid);
-    double2 xim = make_double2(0.0, 0.0);
+    x11 = __ldcs(reinterpret_cast<const double2*>(a11) + tid);
+    x22 = __ldcs(reinterpret_cast<const double2*>(a22) + tid);
+    xre = __ldcs(reinterpret_cast<const double2*>(are) + tid);
     if (CPLX) xim = __ldcs(reinterpret_cast<const double2*>(aim) + tid);
-    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x11.x, x22.x, xre.x, xim.x);
-    const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x11.y, x22.y, xre.y, xim.y);
+  } else if (l0 < r) {  // ragged tail: one matrix
+    x11.x = a11[l0];
+    x22.x = a22[l0];
+    xre.x = are[l0];
+    if (CPLX) xim.x = aim[l0];
+  }
+  const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x11.x, x22.x, xre.x, xim.x, kFull);
+  const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x11.y, x22.y, xre.y, xim.y, kFull);
+  const bool p0 = l0 < r && e0.perm, p1 = l0 + 1 < r && e1.perm;
+  if (l0 + 1 < r) {
     __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
     __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
     __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
     __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
     if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
     if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
-    p0 = e0.perm;
-    p1 = e1.perm;
-  } else if (l0 < r) {  // ragged tail: one matrix
-    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(a11[l0], a22[l0], are[l0], CPLX ? aim[l0] : 0.0);
+  } else if (l0 < r) {
     l1[l0] = e0.l1;
     l2[l0] = e0.l2;
     cs[l0] = e0.c;
     sr[l0] = e0.sr;
     if (CPLX) si[l0] = e0.si;
     if (zeta) zeta[l0] = e0.zeta;
-    p0 = e0.perm;
   }
   if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
     const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
@@ -78,16 +83,17 @@ __global__ void __launch_bounds__(256) evd2_scalar_kernel(
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool p = false;
-  if (l < r) {
-    const Evd2Out e = evd2<CPLX, TAN, NOBACK>(a11[l], a22[l], are[l], CPLX ? aim[l] : 0.0);
+  const bool in = l < r;
+  const Evd2Out e = evd2<CPLX, TAN, NOBACK>(in ? a11[l] : 0.0, in ? a22[l] : 0.0,
+                                            in ? are[l] : 0.0, (CPLX && in) ? aim[l] : 0.0, kFull);
+  const bool p = in && e.perm;
+  if (in) {
     l1[l] = e.l1;
     l2[l] = e.l2;
     cs[l] = e.c;
     sr[l] = e.sr;
     if (CPLX) si[l] = e.si;
     if (zeta) zeta[l] = e.zeta;
-    p = e.perm;
   }
   if (perm) {
     const uint32_t b = __ballot_sync(0xffffffffu, p);
@@ -174,10 +180,10 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
       case 0: q[i] = div_rn(x, y); break;
       case 1: q[i] = __ddiv_rn(x, y); break;
       case 2: q[i] = scalbn_rn(x, static_cast<int>(y)); break;
-      case 3: q[i] = divide_sf<true, true>(x, make_divisor(y)); break;
-      case 4: q[i] = divide_checked(x, make_divisor(y)); break;
+      case 3: q[i] = divide_sf<true, true>(x, make_divisor(y), __activemask()); break;
+      case 4: q[i] = divide_checked(x, make_divisor(y), __activemask()); break;
       case 5: q[i] = hypot_naive(fabs(x), fabs(y)); break;
-      default: q[i] = divide_sf<false, true>(x, make_divisor(y)); break;
+      default: q[i] = divide_sf<false, true>(x, make_divisor(y), __activemask()); break;
     }
   }
 }

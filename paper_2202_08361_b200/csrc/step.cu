@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(T) step_kernel(const StepParams P) {
     if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
       double b11, b22, br, bi;
       gram(zr, zi, ep, fp, eq, fq, b11, b22, br, bi);
-      const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi);
+      const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi, kFull);  // warp 0, all lanes
       if (threadIdx.x == 0) {
         rot[0] = o.c;
         rot[1] = o.sr;
