@@ -181,7 +181,7 @@ __device__ __forceinline__ void ef_from_ssq(int E, double ssq, double& e, double
     g = g * 2.0;
     k -= 1;
   }
-  f = __dsqrt_rn(g);
+  f = sqrt_plain(g);  // g in [1, 4)
   e = static_cast<double>(E + k / 2);
 }
 

@@ -139,3 +139,40 @@ def test_scalbn_full_range():
     ref = np.ldexp(a, k)
     bad = _same(_run(2, a, k.astype(np.float64)), ref)
     assert bad.size == 0, (a[bad[:4]], k[bad[:4]])
+
+
+def test_sqrt_plain_in_range():
+    # the EVD's and the norms' sqrt: arguments in [1, 4) and up to DBL_MAX
+    rng = np.random.default_rng(17)
+    n = 1 << 22
+    xs = [1 + 3 * rng.random(n), np.ldexp(1 + rng.random(n), rng.integers(-969, 1024, n)),
+          np.nextafter(np.ldexp(np.ones(n), rng.integers(-969, 1023, n)), np.inf),
+          np.array([1.0, 2.0, 4.0 - 2.0 ** -50, 1 + 2.0 ** -52, np.finfo(float).max, 2.0 ** -969])]
+    for x in xs:
+        bad = _same(_run(7, x, x), np.sqrt(x))
+        assert bad.size == 0, x[bad[:4]]
+
+
+def test_div_plain_in_range():
+    # the plain division on operands inside its proven range (jsvd.h)
+    rng = np.random.default_rng(19)
+    n = 1 << 22
+    b = np.ldexp(1 + rng.random(n), rng.integers(-1000, 1000, n))
+    q = np.ldexp(1 + rng.random(n), rng.integers(-999, 999, n))
+    a = q * b
+    ok = (np.abs(a) >= 2.0 ** -968) & np.isfinite(a) & (np.abs(a / b) >= 2.0 ** -1000) \
+        & (np.abs(a / b) <= 2.0 ** 1000)
+    a, b = a[ok], b[ok]
+    a[::3] = -a[::3]
+    b[::5] = -b[::5]
+    bad = _same(_run(8, a, b), a / b)
+    assert bad.size == 0, (a[bad[:4]], b[bad[:4]])
+    # structured significands (ties of the Markstein step), unit exponents
+    sig = np.array([1.0, 2.0 - 2.0 ** -52, 1.5, 1.0 + 2.0 ** -52, 1.5 - 2.0 ** -52, 1.25,
+                    1.75 + 2.0 ** -52, 1.0 + 2.0 ** -26, 2.0 - 2.0 ** -26, 1.3333333333333333])
+    A, B = np.meshgrid(np.concatenate([sig, 1 + rng.random(300)]),
+                       np.concatenate([sig, 1 + rng.random(300)]))
+    for ea, eb in ((0, 0), (-968, 0), (500, -400), (0, 999), (-500, -999)):
+        x, y = np.ldexp(A.ravel(), ea), np.ldexp(B.ravel(), eb)
+        bad = _same(_run(8, x, y), x / y)
+        assert bad.size == 0, (ea, eb, x[bad[:4]], y[bad[:4]])
