@@ -20,7 +20,7 @@
 namespace jsvd {
 
 template <bool CPLX, int T, int CL, int NR>
-__global__ void __launch_bounds__(T) step_kernel(const StepParams P) {
+__global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   using E = typename Elem<CPLX>::T;
   constexpr int W = T * CL;
   constexpr int NW = T / 32;
@@ -241,13 +241,16 @@ struct Geo {
   int T, CL, NR;
 };
 
+// W = 256 * CL lanes (CL = 1 ... 16 CTAs of 256 threads), the smallest W with
+// W * NR >= m.  256-thread CTAs at <= 128 registers leave room for two CTAs
+// (of different pairs) per SM, so one pair's loads overlap another's
+// reductions and EVD.  CL = 16 is a non-portable cluster size (opt-in below).
 static Geo pick_geo(bool cplx, int64_t m) {
   const int NR = cplx ? 8 : 16;  // register-resident elements per lane and column
   int64_t need = (m + NR - 1) / NR, W = 256;
   while (W < need) W *= 2;
   if (W > 4096) return Geo{0, 0, 0};
-  const int T = static_cast<int>(W < 512 ? W : 512);
-  return Geo{T, static_cast<int>(W / T), NR};
+  return Geo{256, static_cast<int>(W / 256), NR};
 }
 
 template <typename Kern, typename... Args>
@@ -263,6 +266,10 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, cudaStream_t s
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CL > 1 ? 1 : 0;
+  if (CL > 8) {
+    cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (a != cudaSuccess) return a;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
   note_launch();
   return e;
@@ -273,12 +280,12 @@ static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams&
                                  cudaStream_t st) {
   constexpr int NR = CPLX ? 8 : 16;
   const int64_t grid = npairs * g.CL;
-  if (g.T == 256) return launch_cl(step_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, P);
   switch (g.CL) {
-    case 1: return launch_cl(step_kernel<CPLX, 512, 1, NR>, grid, 512, 1, st, P);
-    case 2: return launch_cl(step_kernel<CPLX, 512, 2, NR>, grid, 512, 2, st, P);
-    case 4: return launch_cl(step_kernel<CPLX, 512, 4, NR>, grid, 512, 4, st, P);
-    case 8: return launch_cl(step_kernel<CPLX, 512, 8, NR>, grid, 512, 8, st, P);
+    case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, P);
+    case 2: return launch_cl(step_kernel<CPLX, 256, 2, NR>, grid, 256, 2, st, P);
+    case 4: return launch_cl(step_kernel<CPLX, 256, 4, NR>, grid, 256, 4, st, P);
+    case 8: return launch_cl(step_kernel<CPLX, 256, 8, NR>, grid, 256, 8, st, P);
+    case 16: return launch_cl(step_kernel<CPLX, 256, 16, NR>, grid, 256, 16, st, P);
   }
   return cudaErrorInvalidValue;
 }
@@ -293,12 +300,12 @@ static cudaError_t launch_colnorm_t(const Geo& g, int64_t m, int64_t n, const do
                                     int64_t ldg, double* ce, double* cf, cudaStream_t st) {
   constexpr int NR = CPLX ? 8 : 16;
   const int64_t grid = n * g.CL;
-  if (g.T == 256) return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, m, G, ldg, ce, cf);
   switch (g.CL) {
-    case 1: return launch_cl(colnorm_kernel<CPLX, 512, 1, NR>, grid, 512, 1, st, m, G, ldg, ce, cf);
-    case 2: return launch_cl(colnorm_kernel<CPLX, 512, 2, NR>, grid, 512, 2, st, m, G, ldg, ce, cf);
-    case 4: return launch_cl(colnorm_kernel<CPLX, 512, 4, NR>, grid, 512, 4, st, m, G, ldg, ce, cf);
-    case 8: return launch_cl(colnorm_kernel<CPLX, 512, 8, NR>, grid, 512, 8, st, m, G, ldg, ce, cf);
+    case 1: return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, m, G, ldg, ce, cf);
+    case 2: return launch_cl(colnorm_kernel<CPLX, 256, 2, NR>, grid, 256, 2, st, m, G, ldg, ce, cf);
+    case 4: return launch_cl(colnorm_kernel<CPLX, 256, 4, NR>, grid, 256, 4, st, m, G, ldg, ce, cf);
+    case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, NR>, grid, 256, 8, st, m, G, ldg, ce, cf);
+    case 16: return launch_cl(colnorm_kernel<CPLX, 256, 16, NR>, grid, 256, 16, st, m, G, ldg, ce, cf);
   }
   return cudaErrorInvalidValue;
 }
