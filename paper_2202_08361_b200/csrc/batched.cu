@@ -2,16 +2,21 @@
 // SVDs (BASELINE configs[3]: 65536 complex 64 x 32), one CTA per matrix, the
 // whole iteration (G and V) resident in shared memory: HBM is touched once to
 // load A and once to store U, V, sigma.  Same arithmetic as jsvd_gesvj with
-// nblocks = n (flat round-robin) and the reduction spec R = (32, 1,
-// [16,8,4,2,1]): lane L of a warp owns rows L, L+32, ... of a pair.
+// nblocks = n (flat round-robin) and the reduction spec R = (16, 1, [8,4,2,1]):
+// lane L of a HALF-warp owns rows L, L+16, ... of a pair, so one warp serves
+// two pairs at once and every shuffle of a reduction serves both.
 //
-// Per step (n/2 pairs):
-//   A  every warp: norms, scaled dot, convergence test of its pairs (Alg 3.1,
-//      3.2; R#14), results to shared memory
-//   B  warp 0: the Grammians and 2x2 EVDs of all transformed pairs of the step,
-//      ONE LANE PER PAIR -- the batch of EVDs of Alg 4.1 line 26 vectorised
-//      across lanes as the paper vectorises it across SIMD lanes
-//   C  every warp: rotation of its pairs' G and V columns (Alg 3.4), M-tilde.
+// Per step (n/2 pairs; 256 threads = 16 half-warps):
+//   A  every half-warp, one pair: exponent max, SSQ of x 2^-E (R#14) and the
+//      dot of the columns prescaled by 2^-e (Alg 3.1) -- only the vector work
+//      and the sums; the per-pair scalar tail goes to B
+//   B  warp 0, ONE LANE PER PAIR: f = sqrt(g), the division of the dot, the
+//      convergence test (Alg 3.2), the Grammian (Alg 3.3) and the 2x2 EVD of
+//      every transformed pair -- the batch of EVDs of Alg 4.1 line 26
+//      vectorised across lanes as the paper vectorises it across SIMD lanes
+//
+//   C  every half-warp, one pair: rotation of its G and V columns (Alg 3.4);
+//      M-tilde tracked by its high word (only floor(lg M-tilde) enters Eq. skr)
 // The Eq. (skr) rescale check runs at every step (flat round-robin, R#21).
 #include <cmath>
 
@@ -20,33 +25,120 @@
 
 namespace jsvd {
 
-constexpr int kBT = 256;  // threads per CTA (8 warps)
+constexpr int kBT = 256;  // threads per CTA (8 warps, 16 half-warps)
 constexpr int kBNW = kBT / 32;
+constexpr int kBNH = kBT / 16;
+constexpr int kBW = 16;  // lanes per pair (R.W)
 
 struct PairSlot {
-  double zr, zi, ep, fp, eq, fq;
-  double c, C, S;
+  double ar, ai;  // sums of the prescaled dot (Alg 3.1 lines 5-6)
+  double gp, gq;  // SSQ significands in [1, 4): f = sqrt(g) (R#14)
+  int ep, eq;     // norm exponents (kIntMin: zero column, R#19)
+  double c, C, S; // rotation (Alg 3.4)
   int transform;
   int pad;
 };
 
-template <bool CPLX>
-__device__ __forceinline__ double warp_sum(double v) {
+// sum over the 16 lanes of each half-warp, xor offsets 8, 4, 2, 1 (R)
+__device__ __forceinline__ double hsum(double v) {
 #pragma unroll
-  for (int o = 16; o >= 1; o /= 2) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 8; o >= 1; o /= 2) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t hmax_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 8; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint64_t hmax_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 8; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
-// x 2^-e for a whole column slice, the two-multiply case taken warp-uniformly
-template <int NR, typename E, typename F>
-__device__ __forceinline__ void scaled_loop(const Pow2& f, F&& body) {
-  if (f.two) {
+__device__ __forceinline__ uint32_t abs_hi(double x) { return hi32(x) & 0x7fffffffu; }
+__device__ __forceinline__ uint32_t hi_max(double x, uint32_t m) { return max(m, abs_hi(x)); }
+__device__ __forceinline__ uint32_t hi_max(double2 x, uint32_t m) {
+  return max(m, max(abs_hi(x.x), abs_hi(x.y)));
+}
+
+// floor(lg max|component|) over the half-warp's column slice x[0..NR):
+// from the high words; a column whose largest component is subnormal (or zero)
+// takes the exact 64-bit path (warp-uniform branch).  kIntMin: zero column.
+template <int NR, typename E>
+__device__ __forceinline__ void col_exponents(const E* xp, const E* xq, int& Ep, int& Eq) {
+  uint32_t hp = 0, hq = 0;
 #pragma unroll
-    for (int j = 0; j < NR; ++j) body(j, true);
-  } else {
-#pragma unroll
-    for (int j = 0; j < NR; ++j) body(j, false);
+  for (int j = 0; j < NR; ++j) {
+    hp = hi_max(xp[j], hp);
+    hq = hi_max(xq[j], hq);
   }
+  hp = hmax_u32(hp);
+  hq = hmax_u32(hq);
+  Ep = static_cast<int>(hp >> 20) - 1023;
+  Eq = static_cast<int>(hq >> 20) - 1023;
+  if (__any_sync(0xffffffffu, hp < 0x00100000u || hq < 0x00100000u)) {
+    uint64_t mp = 0, mq = 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      mp = absmax_bits(xp[j], mp);
+      mq = absmax_bits(xq[j], mq);
+    }
+    mp = hmax_u64(mp);
+    mq = hmax_u64(mq);
+    if (hp < 0x00100000u) Ep = ilogb_or_min(mp);
+    if (hq < 0x00100000u) Eq = ilogb_or_min(mq);
+  }
+}
+
+// e = E + k/2 and g = SSQ 2^-k (k even) from the SSQ of x 2^-E (R#14)
+__device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(ssq));
+  int k = static_cast<int>(b >> 52) - 1023;
+  g = __longlong_as_double(static_cast<long long>((b & 0x000fffffffffffffull) |
+                                                  0x3ff0000000000000ull));
+  if (k & 1) {
+    g = g * 2.0;
+    k -= 1;
+  }
+  e = E + k / 2;
+}
+
+// x 2^-E elementwise with one multiply (n in [-1074, 1023]) or two (the
+// warp-uniform TWO case, n > 1023: tiny columns)
+template <bool TWO>
+__device__ __forceinline__ double sc1(double x, const Pow2& f) {
+  return TWO ? (x * f.a) * f.b : x * f.a;
+}
+template <bool TWO>
+__device__ __forceinline__ double2 sc1(double2 x, const Pow2& f) {
+  return make_double2(sc1<TWO>(x.x, f), sc1<TWO>(x.y, f));
+}
+
+template <bool CPLX, int NR, bool TWO>
+__device__ __forceinline__ void ssq_part(const typename Elem<CPLX>::T* xp,
+                                         const typename Elem<CPLX>::T* xq, int Ep, int Eq,
+                                         int hl, int mi, double& sp, double& sq) {
+  const Pow2 fEp(Ep == kIntMin ? 0 : -Ep), fEq(Eq == kIntMin ? 0 : -Eq);
+  sp = sq = 0.0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if (j * kBW + hl < mi) {
+      sp = ssq_acc(sc1<TWO>(xp[j], fEp), sp);
+      sq = ssq_acc(sc1<TWO>(xq[j], fEq), sq);
+    }
+  }
+}
+
+template <bool CPLX, int NR, bool TWO>
+__device__ __forceinline__ void dot_part(const typename Elem<CPLX>::T* xp,
+                                         const typename Elem<CPLX>::T* xq, int ep, int eq,
+                                         int hl, int mi, double& ar, double& ai) {
+  const Pow2 fP(-ep), fQ(-eq);
+  ar = ai = 0.0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+    if (j * kBW + hl < mi) dot_acc(sc1<TWO>(xq[j], fQ), sc1<TWO>(xp[j], fP), ar, ai);
 }
 
 template <bool CPLX, int NR>
@@ -62,7 +154,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   double* ce = reinterpret_cast<double*>(slots + n / 2);
   double* cf = ce + n;
   uint8_t* sPairs = reinterpret_cast<uint8_t*>(cf + n);  // (n-1) x n/2 pivot pairs (n <= 64)
-  __shared__ unsigned long long sMt, sM0;
+  __shared__ unsigned long long sM0;
+  __shared__ uint32_t sMt;  // high word of M-tilde (its floor(lg) is all Eq. skr uses)
   __shared__ int sT;
   __shared__ uint64_t wred[kBNW];
 
@@ -70,6 +163,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   E* Ag = reinterpret_cast<E*>(A) + b * strideA;
   E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4;
   const int np = static_cast<int>(n / 2);
   const int mi = static_cast<int>(m), ni = static_cast<int>(n);
   // the flat round-robin ordering (R#20), once per CTA
@@ -82,9 +176,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 
   // ---- load A, M0 = max |component| (NaN -> inf), V = I
   uint64_t mx = 0;
-  for (int64_t k = threadIdx.x; k < m * n; k += kBT) {
-    const int64_t j = k / m, i = k % m;
-    const E x = Ag[j * lda + i];
+  for (int k = threadIdx.x; k < mi * ni; k += kBT) {
+    const int j = k / mi, i = k - j * mi;
+    const E x = Ag[static_cast<int64_t>(j) * lda + i];
     sG[k] = x;
     if constexpr (CPLX) {
       mx = max(mx, abs_bits(fmin(fabs(x.x), static_cast<double>(INFINITY))));
@@ -93,8 +187,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
     }
   }
-  for (int64_t k = threadIdx.x; k < n * n; k += kBT) {
-    const int64_t j = k / n, i = k % n;
+  for (int k = threadIdx.x; k < ni * ni; k += kBT) {
+    const int j = k / ni, i = k - j * ni;
     if constexpr (CPLX) sV[k] = make_double2(i == j ? 1.0 : 0.0, 0.0);
     else sV[k] = i == j ? 1.0 : 0.0;
   }
@@ -113,11 +207,11 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   }
   // ---- line 1: s0 = F(m) - floor(lg M0) - 1; G1 = 2^s0 G
   int s = Fm - ilogb_bits(sM0) - 1;
-  for (int64_t k = threadIdx.x; k < m * n; k += kBT) {
+  for (int k = threadIdx.x; k < mi * ni; k += kBT) {
     if constexpr (CPLX) sG[k] = make_double2(scalbn_rn(sG[k].x, s), scalbn_rn(sG[k].y, s));
     else sG[k] = scalbn_rn(sG[k], s);
   }
-  if (threadIdx.x == 0) sMt = static_cast<unsigned long long>(__double_as_longlong(scalbn_rn(M0, s)));
+  if (threadIdx.x == 0) sMt = hi32(scalbn_rn(M0, s));
   __syncthreads();
 
   int C = 0;
@@ -125,97 +219,89 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   for (C = 0; C < max_sweeps; ++C) {
     if (threadIdx.x == 0) sT = 0;
     for (int k = 0; k < ni - 1; ++k) {
-      // ---- line 6: rescale check (every step for flat round-robin)
+      // ---- line 6: rescale check (every step for flat round-robin); M-tilde
+      // is normal here (G is scaled to ~ omega / m), so its high word's
+      // exponent field is floor(lg M-tilde)
       {
-        const int lm = ilogb_bits(sMt);
+        const int lm = static_cast<int>(sMt >> 20) - 1023;
         const int sn = (Kr - lm < 0) ? Fm - lm - 1 : 0;
         if (sn != 0) {  // uniform
           __syncthreads();
-          for (int64_t kk = threadIdx.x; kk < m * n; kk += kBT) {
+          for (int kk = threadIdx.x; kk < mi * ni; kk += kBT) {
             if constexpr (CPLX) sG[kk] = make_double2(scalbn_rn(sG[kk].x, sn), scalbn_rn(sG[kk].y, sn));
             else sG[kk] = scalbn_rn(sG[kk], sn);
           }
-          if (threadIdx.x == 0) {
-            sMt = static_cast<unsigned long long>(__double_as_longlong(
-                scalbn_rn(__longlong_as_double(static_cast<long long>(sMt)), sn)));
-          }
+          if (threadIdx.x == 0) sMt = hi32(scalbn_rn(mkd(sMt, 0u), sn));
           s += sn;
           __syncthreads();
         }
       }
-      // ---- phase A: norms, dot, convergence test (one warp per pair)
-      for (int l = warp; l < np; l += kBNW) {
-        const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
+      // ---- phase A: half-warp per pair: exponent max, SSQ, prescaled dot
+      for (int l0 = 0; l0 < np; l0 += kBNH) {  // uniform trip count: both halves shuffle
+        const int l = l0 + hw;
+        const bool act = l < np;
+        const int p = act ? sPairs[2 * (k * np + l)] : 0;
+        const int q = act ? sPairs[2 * (k * np + l) + 1] : 1;
         const E* gp = sG + p * mi;
         const E* gq = sG + q * mi;
         E xp[NR], xq[NR];
-        uint64_t mp = 0, mq = 0;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          const int i = j * 32 + lane;
+          const int i = j * kBW + hl;
           xp[j] = i < mi ? gp[i] : Elem<CPLX>::zero();
           xq[j] = i < mi ? gq[i] : Elem<CPLX>::zero();
-          mp = absmax_bits(xp[j], mp);
-          mq = absmax_bits(xq[j], mq);
         }
-        const int Ep = __reduce_max_sync(0xffffffffu, ilogb_or_min(mp));
-        const int Eq = __reduce_max_sync(0xffffffffu, ilogb_or_min(mq));
-        double sp = 0.0, sq = 0.0;
-        if (Ep != kIntMin) {
-          const Pow2 f(-Ep);
-          scaled_loop<NR, E>(f, [&](int j, bool) {
-            if (j * 32 + lane < mi) sp = ssq_acc(f(xp[j]), sp);
-          });
-        }
-        if (Eq != kIntMin) {
-          const Pow2 f(-Eq);
-          scaled_loop<NR, E>(f, [&](int j, bool) {
-            if (j * 32 + lane < mi) sq = ssq_acc(f(xq[j]), sq);
-          });
-        }
-        sp = warp_sum<CPLX>(sp);
-        sq = warp_sum<CPLX>(sq);
-        double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
-        if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
-        if (Eq != kIntMin) ef_from_ssq(Eq, sq, eq, fq);
-        double zr = 0.0, zi = 0.0;
-        if (Ep != kIntMin && Eq != kIntMin) {
-          const Pow2 fP(-static_cast<int>(ep)), fQ(-static_cast<int>(eq));
-          double ar = 0.0, ai = 0.0;
-#pragma unroll
-          for (int j = 0; j < NR; ++j)
-            if (j * 32 + lane < mi) dot_acc(fQ(xq[j]), fP(xp[j]), ar, ai);
-          ar = warp_sum<CPLX>(ar);
-          if (CPLX) ai = warp_sum<CPLX>(ai);
-          const Divisor d = make_divisor(fq * fp);
-          zr = divide(ar, d);
-          zi = CPLX ? divide(ai, d) : 0.0;
-        }
-        const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
-        if (lane == 0) {
+        int Ep, Eq;
+        col_exponents<NR>(xp, xq, Ep, Eq);
+        double sp, sq, ar, ai;
+        const bool tiny = Ep < -1022 || Eq < -1022;  // 2^-E needs two factors (incl. zero col)
+        if (__any_sync(0xffffffffu, tiny)) ssq_part<CPLX, NR, true>(xp, xq, Ep, Eq, hl, mi, sp, sq);
+        else ssq_part<CPLX, NR, false>(xp, xq, Ep, Eq, hl, mi, sp, sq);
+        sp = hsum(sp);
+        sq = hsum(sq);
+        int ep = kIntMin, eq = kIntMin;
+        double gpv = 1.0, gqv = 1.0;
+        if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
+        if (Eq != kIntMin) eg_from_ssq(Eq, sq, eq, gqv);
+        const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19
+        const bool two = !zero_col && (ep < -1023 || eq < -1023);
+        if (__any_sync(0xffffffffu, two)) dot_part<CPLX, NR, true>(xp, xq, zero_col ? 0 : ep, zero_col ? 0 : eq, hl, mi, ar, ai);
+        else dot_part<CPLX, NR, false>(xp, xq, zero_col ? 0 : ep, zero_col ? 0 : eq, hl, mi, ar, ai);
+        ar = hsum(ar);
+        if (CPLX) ai = hsum(ai);
+        if (act && hl == 0) {
           PairSlot& sl = slots[l];
-          sl.zr = zr;
-          sl.zi = zi;
+          sl.ar = zero_col ? 0.0 : ar;
+          sl.ai = zero_col ? 0.0 : ai;
+          sl.gp = gpv;
+          sl.gq = gqv;
           sl.ep = ep;
-          sl.fp = fp;
           sl.eq = eq;
-          sl.fq = fq;
-          sl.transform = tol <= az;
         }
       }
       __syncthreads();
-      // ---- phase B: Grammians + EVDs of the step, one lane per pair
+      // ---- phase B: norms' f, the dot's division, convergence test,
+      // Grammian and EVD of the step, one lane per pair
       if (warp == 0) {
         int tcount = 0;
-        for (int l = lane; l < np + (32 - (np % 32)) % 32; l += 32) {
-          // every lane runs (dummy pair past np / for converged pairs) so the
-          // EVD's rare-case votes use the full warp mask
-          const bool tr = l < np && slots[l].transform;
+        for (int l0 = 0; l0 < np; l0 += 32) {
+          const int l = l0 + lane;
+          const bool act = l < np;
+          const PairSlot& s0 = slots[act ? l : 0];
+          const bool zp = s0.ep == kIntMin, zq = s0.eq == kIntMin;
+          const double fp = zp ? 1.0 : sqrt_plain(s0.gp), fq = zq ? 1.0 : sqrt_plain(s0.gq);
+          const double ep = zp ? -INFINITY : static_cast<double>(s0.ep);
+          const double eq = zq ? -INFINITY : static_cast<double>(s0.eq);
+          // z = (ar, ai) / fl(fq fp), fl(fq fp) in [1, 4) (Alg 3.1 line 8)
+          const Divisor d = make_divisor_normal(fq * fp);
+          const double zr = divide_sf<true, false>(s0.ar, d, kFull);
+          const double zi = CPLX ? divide_sf<true, false>(s0.ai, d, kFull) : 0.0;
+          const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
+          const bool tr = act && !(zp || zq) && tol <= az;  // Alg 3.2
           if (__any_sync(kFull, tr)) {
-            const PairSlot& s0 = slots[l < np ? l : 0];
             double b11, b22, br, bi;
-            gram(tr ? s0.zr : 0.0, tr ? s0.zi : 0.0, tr ? s0.ep : 0.0, tr ? s0.fp : 1.0,
-                 tr ? s0.eq : 0.0, tr ? s0.fq : 1.0, b11, b22, br, bi);
+            gram(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
+                 tr ? fq : 1.0, b11, b22, br, bi);
             const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi, kFull);
             if (tr) {
               slots[l].c = o.c;
@@ -223,40 +309,44 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
               slots[l].S = o.si;
             }
           }
+          if (act) slots[l].transform = tr;
           tcount += __popc(__ballot_sync(0xffffffffu, tr));
         }
         if (lane == 0) sT += tcount;
       }
       __syncthreads();
       // ---- phase C: rotations of G and V (Alg 3.4), M-tilde
-      uint64_t Mw = 0;
-      for (int l = warp; l < np; l += kBNW) {
+      uint32_t Mw = 0;
+      for (int l = hw; l < np; l += kBNH) {
         const PairSlot& sl = slots[l];
         if (!sl.transform) continue;
         const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
         const double c = sl.c, Cc = sl.C, S = sl.S;
         E* gp = sG + p * mi;
         E* gq = sG + q * mi;
-        for (int i = lane; i < mi; i += 32) {
-          E a = gp[i], bq = gq[i];
-          rot_elem(a, bq, c, Cc, S);
-          gp[i] = a;
-          gq[i] = bq;
-          Mw = absmax_bits(a, Mw);
-          Mw = absmax_bits(bq, Mw);
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const int i = j * kBW + hl;
+          if (i < mi) {
+            E a = gp[i], bq = gq[i];
+            rot_elem(a, bq, c, Cc, S);
+            gp[i] = a;
+            gq[i] = bq;
+            Mw = hi_max(a, Mw);
+            Mw = hi_max(bq, Mw);
+          }
         }
         E* vp = sV + p * ni;
         E* vq = sV + q * ni;
-        for (int i = lane; i < ni; i += 32) {
+        for (int i = hl; i < ni; i += kBW) {
           E a = vp[i], bq = vq[i];
           rot_elem(a, bq, c, Cc, S);
           vp[i] = a;
           vq[i] = bq;
         }
       }
-#pragma unroll
-      for (int o = 16; o >= 1; o /= 2) Mw = max(Mw, __shfl_xor_sync(0xffffffffu, Mw, o));
-      if (lane == 0 && Mw) atomicMax(&sMt, static_cast<unsigned long long>(Mw));
+      Mw = __reduce_max_sync(0xffffffffu, Mw);
+      if (lane == 0 && Mw > sMt) atomicMax(&sMt, Mw);
       __syncthreads();
     }
     if (sT == 0) {
@@ -266,52 +356,59 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     }
     __syncthreads();
   }
-  // ---- finalize: norms, U = G diag(2^-e / f), sigma, sort
-  for (int64_t j = warp; j < n; j += kBNW) {
-    const E* g = sG + j * m;
+  // ---- finalize: norms with the step's R (R#23),
+  // U = G diag(2^-e / f), sigma, sort
+  for (int j0 = 0; j0 < ni; j0 += kBNH) {  // half-warp per column, uniform trip count
+    const int j = j0 + hw;
+    const bool act = j < ni;
+    const E* g = sG + (act ? j : 0) * mi;
+    E x[NR];
     uint64_t mj = 0;
-    for (int64_t i = lane; i < m; i += 32) mj = absmax_bits(g[i], mj);
-    const int Ej = __reduce_max_sync(0xffffffffu, ilogb_or_min(mj));
+#pragma unroll
+    for (int jj = 0; jj < NR; ++jj) {
+      const int i = jj * kBW + hl;
+      x[jj] = i < mi ? g[i] : Elem<CPLX>::zero();
+      mj = absmax_bits(x[jj], mj);
+    }
+    mj = hmax_u64(mj);
+    const int Ej = ilogb_or_min(mj);
     double sj = 0.0;
     if (Ej != kIntMin) {
       const Pow2 f(-Ej);
 #pragma unroll
-      for (int jj = 0; jj < NR; ++jj) {
-        const int i = jj * 32 + lane;
-        if (i < mi) sj = ssq_acc(f(g[i]), sj);
-      }
+      for (int jj = 0; jj < NR; ++jj)
+        if (jj * kBW + hl < mi) sj = ssq_acc(f(x[jj]), sj);
     }
-    sj = warp_sum<CPLX>(sj);
+    sj = hsum(sj);
     double e = -INFINITY, f = 1.0;
     if (Ej != kIntMin) ef_from_ssq(Ej, sj, e, f);
-    if (lane == 0) {
+    if (act && hl == 0) {
       ce[j] = e;
       cf[j] = f;
     }
   }
   __syncthreads();
-  for (int64_t r0 = warp; r0 < n; r0 += kBNW) {
+  for (int r0 = warp; r0 < ni; r0 += kBNW) {
     // output column r0 <- input column j with rank r0
-    int64_t jsel = 0;
-    for (int64_t j = lane; j < n; j += 32) {
+    int jsel = 0;
+    for (int j = lane; j < ni; j += 32) {
       const double ej = ce[j], fj = cf[j];
-      int64_t rank = 0;
-      for (int64_t kk = 0; kk < n; ++kk) {
+      int rank = 0;
+      for (int kk = 0; kk < ni; ++kk) {
         const double ek = ce[kk], fk = cf[kk];
         rank += ((ek > ej) || (ek == ej && (fk > fj || (fk == fj && kk < j)))) ? 1 : 0;
       }
       if (rank == r0) jsel = j + 1;
     }
-#pragma unroll
-    for (int o = 16; o >= 1; o /= 2) jsel = max(jsel, __shfl_xor_sync(0xffffffffu, jsel, o));
-    const int64_t j = jsel - 1;
+    jsel = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(jsel));
+    const int j = jsel - 1;
     const double e = ce[j], f = cf[j];
     const bool fin = !isinf(e);
     const Pow2 sc(fin ? -static_cast<int>(e) : 0);
     const Divisor d = make_divisor(f);
-    E* ucol = Ag + r0 * lda;
-    const E* g = sG + j * m;
-    for (int64_t i = lane; i < m; i += 32) {
+    E* ucol = Ag + static_cast<int64_t>(r0) * lda;
+    const E* g = sG + j * mi;
+    for (int i = lane; i < mi; i += 32) {
       E x = g[i];
       if (fin) {
         if constexpr (CPLX) x = make_double2(divide(sc(x.x), d), divide(sc(x.y), d));
@@ -319,8 +416,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       }
       ucol[i] = x;
     }
-    E* vcol = Vb + r0 * ldv;
-    for (int64_t i = lane; i < n; i += 32) vcol[i] = sV[j * n + i];
+    E* vcol = Vb + static_cast<int64_t>(r0) * ldv;
+    for (int i = lane; i < ni; i += 32) vcol[i] = sV[j * ni + i];
     if (lane == 0) {
       const double es = fin ? e - s : e;
       sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
@@ -376,13 +473,13 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                                            Fm, Kr, tol);
   };
   if (cplx) {
-    if (m <= 32) go(batched_svd_kernel<true, 1>);
-    else if (m <= 64) go(batched_svd_kernel<true, 2>);
-    else go(batched_svd_kernel<true, 4>);
+    if (m <= 32) go(batched_svd_kernel<true, 2>);
+    else if (m <= 64) go(batched_svd_kernel<true, 4>);
+    else go(batched_svd_kernel<true, 8>);
   } else {
-    if (m <= 32) go(batched_svd_kernel<false, 1>);
-    else if (m <= 64) go(batched_svd_kernel<false, 2>);
-    else go(batched_svd_kernel<false, 4>);
+    if (m <= 32) go(batched_svd_kernel<false, 2>);
+    else if (m <= 64) go(batched_svd_kernel<false, 4>);
+    else go(batched_svd_kernel<false, 8>);
   }
   note_launch();
   e = cudaGetLastError();
@@ -393,10 +490,10 @@ extern "C" jsvd_status jsvd_batched_rspec(jsvd_dtype dt, int64_t m, int32_t* W, 
                                           int32_t* offs, int32_t* noffs) {
   if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || m > 128 || !W || !c || !offs || !noffs)
     return JSVD_EINVAL;
-  *W = 32;
+  *W = kBW;
   *c = 1;
   int k = 0;
-  for (int o = 16; o >= 1; o /= 2) offs[k++] = o;
+  for (int o = kBW / 2; o >= 1; o /= 2) offs[k++] = o;
   *noffs = k;
   return JSVD_OK;
 }
