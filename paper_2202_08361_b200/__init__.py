@@ -66,7 +66,9 @@ def lib():
                                  _i32, ct.POINTER(_i32), _vp, _vp, ct.c_size_t, _vp]
         L.jsvd_gesvj_batched.restype = ct.c_int
         L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
-                                         _i64, _vp, _i32, _vp, _vp, _vp]
+                                         _i64, _vp, _i32, _vp, _vp, _vp, _vp]
+        L.jsvd_fp64_peak.restype = ct.c_int
+        L.jsvd_fp64_peak.argtypes = [_i32, _i64, _vp, ct.POINTER(_i64), _vp]
         L.jsvd_maxnorm.restype = ct.c_int
         L.jsvd_maxnorm.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp]
         L.jsvd_scale.restype = ct.c_int
@@ -279,10 +281,13 @@ def gesvj(A, nblocks=None, max_sweeps=30, V=None, work=None, stream=None):
                 tps=[tps[k] for k in range(sw.value)], status=st)
 
 
-def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None, stream=None):
+def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None, stream=None,
+                  transforms=None):
     """A: (batch, m, n) CUDA tensor whose matrices are column-major, i.e.
     A.stride() == (m*n, 1, m) (use X.transpose(1,2).contiguous().transpose(1,2)).
-    In place: A becomes U.  Returns dict(U, V, sigma, sweeps, status)."""
+    In place: A becomes U.  Returns dict(U, V, sigma, sweeps, status, transforms)
+    (transforms: int64 per matrix, the number of transformed pair-steps, only
+    when a tensor is passed)."""
     b, m, n = A.shape
     if A.dtype not in (torch.float64, torch.complex128) or A.stride(1) != 1 or A.stride(2) < m:
         raise ValueError("A must be float64/complex128 with column-major matrices")
@@ -295,6 +300,26 @@ def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None
     status = torch.empty(b, dtype=torch.int32, device=dev) if status is None else status
     st = lib().jsvd_gesvj_batched(C64 if cplx else R64, b, m, n, _p(A), A.stride(2), A.stride(0),
                                   _p(V), V.stride(2), V.stride(0), _p(sigma), max_sweeps,
-                                  _p(sweeps), _p(status), _stream(stream))
+                                  _p(sweeps), _p(status),
+                                  _p(transforms) if transforms is not None else None,
+                                  _stream(stream))
     _check(st, "jsvd_gesvj_batched")
-    return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status)
+    return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status, transforms=transforms)
+
+
+def fp64_peak(iters=4096, blocks=None, stream=None):
+    """Measured FP64 pipe throughput (DFMA instructions per second, thread
+    level) of jsvd_fp64_peak, timed with CUDA events on `stream`."""
+    dev = torch.cuda.current_device()
+    if blocks is None:
+        blocks = 8 * torch.cuda.get_device_properties(dev).multi_processor_count
+    out = torch.empty(blocks * 256, dtype=torch.float64, device="cuda")
+    cnt = _i64()
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(lib().jsvd_fp64_peak(blocks, 64, _p(out), ct.byref(cnt), s.cuda_stream), "jsvd_fp64_peak")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    _check(lib().jsvd_fp64_peak(blocks, iters, _p(out), ct.byref(cnt), s.cuda_stream), "jsvd_fp64_peak")
+    e1.record(s)
+    s.synchronize()
+    return cnt.value / (e0.elapsed_time(e1) / 1e3)

@@ -145,7 +145,7 @@ template <bool CPLX, int NR>
 __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
-    int Fm, int Kr, double tol) {
+    int64_t* transforms_out, int Fm, int Kr, double tol) {
   using E = typename Elem<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* sG = reinterpret_cast<E*>(smem_raw);
@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     if (threadIdx.x == 0) {
       if (status_out) status_out[b] = isinf(M0) ? JSVD_ENONFINITE : JSVD_ERANK;
       if (sweeps_out) sweeps_out[b] = 0;
+      if (transforms_out) transforms_out[b] = 0;
     }
     return;
   }
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   __syncthreads();
 
   int C = 0;
+  int64_t Ttot = 0;  // transformed pair-steps (thread 0)
   bool converged = false;
   for (C = 0; C < max_sweeps; ++C) {
     if (threadIdx.x == 0) sT = 0;
@@ -349,6 +351,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       if (lane == 0 && Mw > sMt) atomicMax(&sMt, Mw);
       __syncthreads();
     }
+    if (threadIdx.x == 0) Ttot += sT;
     if (sT == 0) {
       converged = true;
       ++C;
@@ -426,6 +429,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   if (threadIdx.x == 0) {
     if (status_out) status_out[b] = converged ? JSVD_OK : JSVD_ENOCONV;
     if (sweeps_out) sweeps_out[b] = C;
+    if (transforms_out) transforms_out[b] = Ttot;
   }
 }
 
@@ -451,7 +455,7 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                           double* A, int64_t lda, int64_t strideA, double* V,
                                           int64_t ldv, int64_t strideV, double* sigma,
                                           int32_t max_sweeps, int32_t* sweeps_done,
-                                          int32_t* status, void* stream) {
+                                          int32_t* status, int64_t* transforms, void* stream) {
   const bool cplx = dt == JSVD_C64;
   if ((dt != JSVD_R64 && dt != JSVD_C64) || batch < 0 || m < n || n < 2 || (n & 1) || m > 128 ||
       n > 64 || lda < m || ldv < n || strideA < lda * n || strideV < ldv * n || max_sweeps < 0 ||
@@ -470,7 +474,7 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<static_cast<unsigned>(batch), kBT, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
                                                            sigma, max_sweeps, sweeps_done, status,
-                                                           Fm, Kr, tol);
+                                                           transforms, Fm, Kr, tol);
   };
   if (cplx) {
     if (m <= 32) go(batched_svd_kernel<true, 2>);
