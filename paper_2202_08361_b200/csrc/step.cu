@@ -133,6 +133,23 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
   const bool transform = P.tol <= az;
 
+  // V columns of a transformed pair: the first NV rows per lane are loaded
+  // now, so their latency overlaps the Grammian + EVD of warp 0
+  constexpr int NV = 2;
+  E va[NV], vb[NV];
+  E* vp = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(p) * P.ldv;
+  E* vq = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(q) * P.ldv;
+  if (transform && P.V) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int64_t i = static_cast<int64_t>(j) * W + L;
+      if (i < P.n) {
+        va[j] = vp[i];
+        vb[j] = vq[i];
+      }
+    }
+  }
+
   uint64_t Mloc = 0;
   if (transform) {
     if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
@@ -168,9 +185,16 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   if (transform) {
     if (P.V) {
       const double c = rot[0], C = rot[1], S = rot[2];
-      E* vp = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(p) * P.ldv;
-      E* vq = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(q) * P.ldv;
-      for (int64_t i = L; i < P.n; i += W) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int64_t i = static_cast<int64_t>(j) * W + L;
+        if (i < P.n) {
+          rot_elem(va[j], vb[j], c, C, S);
+          vp[i] = va[j];
+          vq[i] = vb[j];
+        }
+      }
+      for (int64_t i = NV * W + L; i < P.n; i += W) {
         E a = vp[i], b = vq[i];
         rot_elem(a, b, c, C, S);
         vp[i] = a;
