@@ -56,11 +56,6 @@ __device__ __forceinline__ uint64_t hmax_u64(uint64_t v) {
   return v;
 }
 
-__device__ __forceinline__ uint32_t abs_hi(double x) { return hi32(x) & 0x7fffffffu; }
-__device__ __forceinline__ uint32_t hi_max(double x, uint32_t m) { return max(m, abs_hi(x)); }
-__device__ __forceinline__ uint32_t hi_max(double2 x, uint32_t m) {
-  return max(m, max(abs_hi(x.x), abs_hi(x.y)));
-}
 
 // floor(lg max|component|) over the half-warp's column slice x[0..NR):
 // from the high words; a column whose largest component is subnormal (or zero)
@@ -102,43 +97,6 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
     k -= 1;
   }
   e = E + k / 2;
-}
-
-// x 2^-E elementwise with one multiply (n in [-1074, 1023]) or two (the
-// warp-uniform TWO case, n > 1023: tiny columns)
-template <bool TWO>
-__device__ __forceinline__ double sc1(double x, const Pow2& f) {
-  return TWO ? (x * f.a) * f.b : x * f.a;
-}
-template <bool TWO>
-__device__ __forceinline__ double2 sc1(double2 x, const Pow2& f) {
-  return make_double2(sc1<TWO>(x.x, f), sc1<TWO>(x.y, f));
-}
-
-template <bool CPLX, int NR, bool TWO>
-__device__ __forceinline__ void ssq_part(const typename Elem<CPLX>::T* xp,
-                                         const typename Elem<CPLX>::T* xq, int Ep, int Eq,
-                                         int hl, int mi, double& sp, double& sq) {
-  const Pow2 fEp(Ep == kIntMin ? 0 : -Ep), fEq(Eq == kIntMin ? 0 : -Eq);
-  sp = sq = 0.0;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    if (j * kBW + hl < mi) {
-      sp = ssq_acc(sc1<TWO>(xp[j], fEp), sp);
-      sq = ssq_acc(sc1<TWO>(xq[j], fEq), sq);
-    }
-  }
-}
-
-template <bool CPLX, int NR, bool TWO>
-__device__ __forceinline__ void dot_part(const typename Elem<CPLX>::T* xp,
-                                         const typename Elem<CPLX>::T* xq, int ep, int eq,
-                                         int hl, int mi, double& ar, double& ai) {
-  const Pow2 fP(-ep), fQ(-eq);
-  ar = ai = 0.0;
-#pragma unroll
-  for (int j = 0; j < NR; ++j)
-    if (j * kBW + hl < mi) dot_acc(sc1<TWO>(xq[j], fQ), sc1<TWO>(xp[j], fP), ar, ai);
 }
 
 template <bool CPLX, int NR>
@@ -255,10 +213,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
         }
         int Ep, Eq;
         col_exponents<NR>(xp, xq, Ep, Eq);
-        double sp, sq, ar, ai;
-        const bool tiny = Ep < -1022 || Eq < -1022;  // 2^-E needs two factors (incl. zero col)
-        if (__any_sync(0xffffffffu, tiny)) ssq_part<CPLX, NR, true>(xp, xq, Ep, Eq, hl, mi, sp, sq);
-        else ssq_part<CPLX, NR, false>(xp, xq, Ep, Eq, hl, mi, sp, sq);
+        double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
+        double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
         sp = hsum(sp);
         sq = hsum(sq);
         int ep = kIntMin, eq = kIntMin;
@@ -266,9 +222,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
         if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
         if (Eq != kIntMin) eg_from_ssq(Eq, sq, eq, gqv);
         const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19
-        const bool two = !zero_col && (ep < -1023 || eq < -1023);
-        if (__any_sync(0xffffffffu, two)) dot_part<CPLX, NR, true>(xp, xq, zero_col ? 0 : ep, zero_col ? 0 : eq, hl, mi, ar, ai);
-        else dot_part<CPLX, NR, false>(xp, xq, zero_col ? 0 : ep, zero_col ? 0 : eq, hl, mi, ar, ai);
+        double ar = 0.0, ai = 0.0;
+        if (!zero_col) dot_lane<NR>(xq, xp, eq, ep, ar, ai);
         ar = hsum(ar);
         if (CPLX) ai = hsum(ai);
         if (act && hl == 0) {
@@ -304,7 +259,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
             double b11, b22, br, bi;
             gram(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
                  tr ? fq : 1.0, b11, b22, br, bi);
-            const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi, kFull);
+            const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);
             if (tr) {
               slots[l].c = o.c;
               slots[l].C = o.sr;
@@ -326,6 +281,11 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
         const double c = sl.c, Cc = sl.C, S = sl.S;
         E* gp = sG + p * mi;
         E* gq = sG + q * mi;
+        // M-tilde only matters once it reaches 2^(K+1) (Eq. skr): every
+        // component after the rotation is below 2^(max(e_p,e_q) + 1.5), so a
+        // pair with max(e) <= K - 1 is not tracked (same checks and rescales
+        // as the exact M; see step.cu)
+        const bool track = max(sl.ep, sl.eq) > Kr - 1;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
           const int i = j * kBW + hl;
@@ -334,8 +294,10 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
             rot_elem(a, bq, c, Cc, S);
             gp[i] = a;
             gq[i] = bq;
-            Mw = hi_max(a, Mw);
-            Mw = hi_max(bq, Mw);
+            if (track) {
+              Mw = hi_max(a, Mw);
+              Mw = hi_max(bq, Mw);
+            }
           }
         }
         E* vp = sV + p * ni;

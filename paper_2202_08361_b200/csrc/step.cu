@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   __shared__ RedSlot<NW, int> rs_e;
   __shared__ RedSlot<NW, double> rs_ssq;
   __shared__ RedSlot<NW, double> rs_dot;
-  __shared__ uint64_t rs_m[NW];
+  __shared__ uint32_t rs_m[NW];
   __shared__ double rot[3];
 
   const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
@@ -81,29 +81,18 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
   }
 
-  // ---- spade: E = floor(lg max |component|) per column
-  uint64_t mp = 0, mq = 0;
+  // ---- spade: E = floor(lg max |component|) per column (high words)
+  uint32_t hp = 0, hq = 0;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
-    mp = absmax_bits(xp[j], mp);
-    mq = absmax_bits(xq[j], mq);
+    hp = hi_max(xp[j], hp);
+    hq = hi_max(xq[j], hq);
   }
-  int Ep = ilogb_or_min(mp), Eq = ilogb_or_min(mq);
+  int Ep = lane_exponent<NR>(hp, xp), Eq = lane_exponent<NR>(hq, xq);
   tree_max2i<T, CL>(Ep, Eq, rs_e);
-  // ---- spade: SSQ of x 2^-E in the lane order of R
-  double sp = 0.0, sq = 0.0;
-  if (Ep != kIntMin) {
-    const Pow2 f(-Ep);
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-      if (static_cast<int64_t>(j) * W + L < P.m) sp = ssq_acc(f(xp[j]), sp);
-  }
-  if (Eq != kIntMin) {
-    const Pow2 f(-Eq);
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-      if (static_cast<int64_t>(j) * W + L < P.m) sq = ssq_acc(f(xq[j]), sq);
-  }
+  // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform)
+  double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
+  double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
   tree_sum2<T, CL>(sp, sq, rs_ssq);
   double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
   if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
@@ -117,18 +106,18 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
 
   // ---- club: a21' = (g_q 2^-e_q)^* (g_p 2^-e_p) / fl(f_q f_p)  (Alg 3.1)
   double zr = 0.0, zi = 0.0;
-  const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19
+  const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19 (cluster-uniform)
   if (!zero_col) {
-    const Pow2 fP(-static_cast<int>(ep)), fQ(-static_cast<int>(eq));
-    double ar = 0.0, ai = 0.0;
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-      if (static_cast<int64_t>(j) * W + L < P.m) dot_acc(fQ(xq[j]), fP(xp[j]), ar, ai);
+    double ar, ai;
+    dot_lane<NR>(xq, xp, static_cast<int>(eq), static_cast<int>(ep), ar, ai);
     tree_sum2<T, CL>(ar, ai, rs_dot);
-    const Divisor d = make_divisor(fq * fp);
-    zr = divide(ar, d);
-    zi = CPLX ? divide(ai, d) : 0.0;
+    const Divisor d = make_divisor_normal(fq * fp);  // in [1, 4)
+    zr = divide_sf<true, false>(ar, d, kFull);
+    zi = CPLX ? divide_sf<true, false>(ai, d, kFull) : 0.0;
   }
+  // the last read of a peer CTA's shared memory is done: arrive now, wait at
+  // exit (the wait keeps this CTA's slots alive for its peers)
+  if constexpr (CL > 1) __cluster_barrier_arrive();
   // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
   const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
   const bool transform = P.tol <= az;
@@ -150,12 +139,11 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
   }
 
-  uint64_t Mloc = 0;
   if (transform) {
     if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
       double b11, b22, br, bi;
       gram(zr, zi, ep, fp, eq, fq, b11, b22, br, bi);
-      const Evd2Out o = evd2<CPLX, true, true>(b11, b22, br, bi, kFull);  // warp 0, all lanes
+      const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);  // warp 0, all lanes
       if (threadIdx.x == 0) {
         rot[0] = o.c;
         rot[1] = o.sr;
@@ -164,13 +152,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
     __syncthreads();
     const double c = rot[0], C = rot[1], S = rot[2];
-    // ---- star: rotate the register-resident pair, track max |component|
+    // ---- star: rotate the register-resident pair
 #pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      rot_elem(xp[j], xq[j], c, C, S);
-      Mloc = absmax_bits(xp[j], Mloc);
-      Mloc = absmax_bits(xq[j], Mloc);
-    }
+    for (int j = 0; j < NR; ++j) rot_elem(xp[j], xq[j], c, C, S);
   }
   if (transform || sn != 0) {
 #pragma unroll
@@ -201,11 +185,32 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
         vq[i] = b;
       }
     }
-    const uint64_t Mc = cta_max_u64<T>(Mloc, rs_m);
-    if (threadIdx.x == 0) {
-      atomicMax(P.Mt ? &P.Mt[(P.slot + 1) % 3] : P.mmax, static_cast<unsigned long long>(Mc));
-      if (crank == 0) atomicAdd(P.t_dev, 1ull);
+    // ---- M: max |component| of the transformed pair.  In the driver
+    // (Mt) only floor(lg M-tilde) >= K + 1 matters (Eq. skr): every component
+    // is below sqrt(|g_p|^2 + |g_q|^2) <= 2^(max(e_p,e_q) + 1.5), so a pair
+    // with max(e) <= K - 1 cannot reach 2^(K+1) and is not tracked; an
+    // untracked M only lowers M-tilde while it stays below 2^(K+1), so every
+    // check and every rescale is the same as with the exact M.  Otherwise the
+    // exact max: high words first (one CTA reduction), then the low words of
+    // the lanes holding the largest high word, straight to the atomic.
+    const bool track = !P.Mt || fmax(ep, eq) > static_cast<double>(P.Kr - 1);
+    if (track) {
+      uint32_t hm = 0;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        hm = hi_max(xp[j], hm);
+        hm = hi_max(xq[j], hm);
+      }
+      const uint32_t H = cta_max_u32<T>(hm, rs_m);
+      if (hm == H && H != 0u) {
+        uint32_t lmax = 0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) lmax = lo_max_at(xp[j], H, lo_max_at(xq[j], H, lmax));
+        const unsigned long long Mx = (static_cast<unsigned long long>(H) << 32) | lmax;
+        atomicMax(P.Mt ? &P.Mt[(P.slot + 1) % 3] : P.mmax, Mx);
+      }
     }
+    if (threadIdx.x == 0 && crank == 0) atomicAdd(P.t_dev, 1ull);
   }
   if (P.Mt && pair == 0 && lead) {  // M-tilde / s bookkeeping for the next step
     const double cur = __longlong_as_double(static_cast<long long>(mt_cur));
@@ -215,7 +220,10 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     P.Mt[(P.slot + 2) % 3] = 0ull;
     P.s_slots[(P.slot + 1) % 3] = P.s_slots[P.slot] + sn;
   }
-  if constexpr (CL > 1) cg::this_cluster().sync();  // keep DSMEM alive for peers
+  if constexpr (CL > 1) {
+    if (zero_col) __cluster_barrier_arrive();  // (no dot: arrive here)
+    __cluster_barrier_wait();  // keep this CTA's shared memory alive for its peers
+  }
 }
 
 // ---- finalize helpers ---------------------------------------

@@ -40,6 +40,13 @@ __device__ __forceinline__ double pow2_any(int n) {
   return n >= -1022 ? pow2i(n) : __longlong_as_double(1ll << (n + 1074));
 }
 
+__device__ __forceinline__ double scale1(double x, double a) { return x * a; }
+__device__ __forceinline__ double2 scale1(double2 x, double a) { return make_double2(x.x * a, x.y * a); }
+__device__ __forceinline__ double scale2(double x, double a, double b) { return (x * a) * b; }
+__device__ __forceinline__ double2 scale2(double2 x, double a, double b) {
+  return make_double2((x.x * a) * b, (x.y * a) * b);
+}
+
 // x * 2^n with one rounding for n in [-1074, 2046] (R#3): one multiply, or two
 // when n > 1023 (the first, an upscaling, is exact).
 struct Pow2 {
@@ -166,8 +173,45 @@ __device__ __forceinline__ uint64_t cta_max_u64(uint64_t v, uint64_t* warp_slots
   return fold<T / 32>(warp_slots, MaxU64Op());
 }
 
+// CTA-wide max of a u32, every thread gets it
+template <int T>
+__device__ __forceinline__ uint32_t cta_max_u32(uint32_t v, uint32_t* warp_slots) {
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) warp_slots[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t r = warp_slots[0];
+#pragma unroll
+  for (int w = 1; w < T / 32; ++w) r = max(r, warp_slots[w]);
+  return r;
+}
+// max of m and the low words of the components whose |high word| is H
+__device__ __forceinline__ uint32_t lo_max_at(double x, uint32_t H, uint32_t m) {
+  return (hi32(x) & 0x7fffffffu) == H ? max(m, lo32(x)) : m;
+}
+__device__ __forceinline__ uint32_t lo_max_at(double2 x, uint32_t H, uint32_t m) {
+  return lo_max_at(x.y, H, lo_max_at(x.x, H, m));
+}
+
 // floor(lg max|x|) of the lane's elements as an int (kIntMin if all zero)
 __device__ __forceinline__ int ilogb_or_min(uint64_t b) { return b ? ilogb_bits(b) : kIntMin; }
+
+// |x| high words: their max carries floor(lg max|x|) unless it is subnormal
+__device__ __forceinline__ uint32_t abs_hi(double x) { return hi32(x) & 0x7fffffffu; }
+__device__ __forceinline__ uint32_t hi_max(double x, uint32_t m) { return max(m, abs_hi(x)); }
+__device__ __forceinline__ uint32_t hi_max(double2 x, uint32_t m) {
+  return max(m, max(abs_hi(x.x), abs_hi(x.y)));
+}
+// floor(lg max|component|) of a lane's NR elements from their high-word max h;
+// a lane whose largest component is subnormal (or zero) takes the exact path
+template <int NR, typename E>
+__device__ __forceinline__ int lane_exponent(uint32_t h, const E* x) {
+  if (h >= 0x00100000u) return static_cast<int>(h >> 20) - 1023;
+  uint64_t m = 0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) m = absmax_bits(x[j], m);
+  return ilogb_or_min(m);
+}
+
 
 // (e, f) of a column from E = floor(lg max) and the total SSQ of x 2^-E
 // (R#14): k = logb(SSQ), g = SSQ 2^-k, odd k -> (2g, k-1),
@@ -201,6 +245,45 @@ __device__ __forceinline__ void dot_acc(double2 q, double2 p, double& ar, double
   ai = fma(q.x, p.y, ai);
   ar = fma(q.y, p.y, ar);
   ai = fma(-q.y, p.x, ai);
+}
+
+// SSQ of x 2^-E over a lane's NR elements in increasing index (R#14); E is
+// uniform over the caller's group, so the two-multiply case (2^-E not
+// representable: E < -1023) is a uniform branch.  Zero-filled padding adds
+// exact zeros to a non-negative sum.
+template <int NR, typename E>
+__device__ __forceinline__ double ssq_lane(const E* x, int Ex) {
+  double s = 0.0;
+  if (-Ex > 1023) {
+    const double a = 0x1p1023, b = pow2i(-Ex - 1023);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s = ssq_acc(scale2(x[j], a, b), s);
+  } else {
+    const double a = pow2_any(-Ex);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s = ssq_acc(scale1(x[j], a), s);
+  }
+  return s;
+}
+
+// Alg 3.1 lines 5-6 over a lane's NR elements with the prescale 2^-e (e
+// uniform over the caller's group; two multiplies only when 2^-e is not
+// representable).  Zero padding adds exact zeros (at most the sign of a zero
+// partial sum changes, which no output depends on: z = 0 is never transformed).
+template <int NR, typename E>
+__device__ __forceinline__ void dot_lane(const E* xq, const E* xp, int eq, int ep, double& ar,
+                                         double& ai) {
+  ar = ai = 0.0;
+  if (-eq > 1023 || -ep > 1023) {
+    const Pow2 fQ(-eq), fP(-ep);
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      dot_acc(scale2(xq[j], fQ.a, fQ.b), scale2(xp[j], fP.a, fP.b), ar, ai);
+  } else {
+    const double aq = pow2_any(-eq), ap = pow2_any(-ep);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
+  }
 }
 
 // Alg 3.4 with P = I: x_p' = fma(x_q, e', x_p) c, x_q' = fma(x_p, -conj(e'), x_q) c
