@@ -445,7 +445,7 @@ class StepC64Workload(StepWorkload):
         self.mm = torch.zeros(1, dtype=torch.float64, device="cuda")
         self.k = 0
         self.units_per_step = 1
-        self.kernel = "step_kernel<1,256,16,8>"
+        self.kernel = "step_kernel<1,256,8,4,12>"
         self.l2_note = "G 4.3 GB + V 1.1 GB >> L2"
 
     def bytes_for(self, steps, transformed):
@@ -515,7 +515,7 @@ class DistC64Workload:
         self.k = 0
         self.world = world
         self.units_per_step = 1.0 / world  # value = world * units * steps / time = global steps/s
-        self.kernel = "step_kernel<1,256,16,8>"
+        self.kernel = "step_kernel<1,256,8,4,12>"
         self.l2_note = "local G + V >> L2"
 
     def prepare(self):

@@ -19,7 +19,31 @@
 
 namespace jsvd {
 
-template <bool CPLX, int T, int CL, int NR>
+// 16-byte / 8-byte asynchronous global -> shared copies (LDGSTS), zero-filled
+// past the end of the column (src_size 0)
+__device__ __forceinline__ void cp_async_el(double2* dst, const double2* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_el(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+__device__ __forceinline__ double scalbn_el(double x, int n) { return scalbn_rn(x, n); }
+__device__ __forceinline__ double2 scalbn_el(double2 x, int n) {
+  return make_double2(scalbn_rn(x.x, n), scalbn_rn(x.y, n));
+}
+
+// Lane L of the W = T*CL lanes holds rows j*W + L of both columns: j < NR in
+// registers, NR <= j < NR+NS in shared memory (NS > 0 for the longest columns:
+// twice the rows per lane at the same register count, so a pair needs half the
+// CTAs and twice as many pairs are resident).  Every pass walks j upwards, so
+// the per-lane accumulation order of R is unchanged.
+template <bool CPLX, int T, int CL, int NR, int NS>
 __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   using E = typename Elem<CPLX>::T;
   constexpr int W = T * CL;
@@ -29,6 +53,10 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   __shared__ RedSlot<NW, double> rs_dot;
   __shared__ uint32_t rs_m[NW];
   __shared__ double rot[3];
+  extern __shared__ __align__(16) unsigned char step_smem[];
+  E* sx = reinterpret_cast<E*>(step_smem);  // [NS][2][T]
+  const auto sP = [&](int j) -> E& { return sx[(2 * j) * T + threadIdx.x]; };
+  const auto sQ = [&](int j) -> E& { return sx[(2 * j + 1) * T + threadIdx.x]; };
 
   const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
   const int64_t pair = blockIdx.x / CL;
@@ -43,6 +71,16 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   E* gp = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(p) * P.ldg;
   E* gq = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(q) * P.ldg;
   const bool lead = (crank == 0) && (threadIdx.x == 0);
+
+  // the shared-memory rows first (asynchronous), then the register rows
+#pragma unroll 2
+  for (int j = 0; j < NS; ++j) {
+    const int64_t i = static_cast<int64_t>(NR + j) * W + L;
+    const bool ok = i < P.m;
+    cp_async_el(&sP(j), gp + (ok ? i : 0), ok);
+    cp_async_el(&sQ(j), gq + (ok ? i : 0), ok);
+  }
+  if constexpr (NS > 0) asm volatile("cp.async.commit_group;\n" ::);
 
   // rescale check (Alg 4.1 line 6; Eqs. skn/skr; R#21): every step touches all
   // n columns, so each pair scales its own two columns on load.
@@ -68,16 +106,17 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       xq[j] = Elem<CPLX>::zero();
     }
   }
+  if constexpr (NS > 0) cp_async_wait_all();  // each thread reads only its own slots
   if (sn != 0) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      if constexpr (CPLX) {
-        xp[j] = make_double2(scalbn_rn(xp[j].x, sn), scalbn_rn(xp[j].y, sn));
-        xq[j] = make_double2(scalbn_rn(xq[j].x, sn), scalbn_rn(xq[j].y, sn));
-      } else {
-        xp[j] = scalbn_rn(xp[j], sn);
-        xq[j] = scalbn_rn(xq[j], sn);
-      }
+      xp[j] = scalbn_el(xp[j], sn);
+      xq[j] = scalbn_el(xq[j], sn);
+    }
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      sP(j) = scalbn_el(sP(j), sn);
+      sQ(j) = scalbn_el(sQ(j), sn);
     }
   }
 
@@ -88,11 +127,67 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     hp = hi_max(xp[j], hp);
     hq = hi_max(xq[j], hq);
   }
-  int Ep = lane_exponent<NR>(hp, xp), Eq = lane_exponent<NR>(hq, xq);
+#pragma unroll 2
+  for (int j = 0; j < NS; ++j) {
+    hp = hi_max(sP(j), hp);
+    hq = hi_max(sQ(j), hq);
+  }
+  int Ep, Eq;
+  if (hp >= 0x00100000u) {
+    Ep = static_cast<int>(hp >> 20) - 1023;
+  } else {  // largest component subnormal or zero: exact from the bit patterns
+    uint64_t mb = 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) mb = absmax_bits(xp[j], mb);
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) mb = absmax_bits(sP(j), mb);
+    Ep = ilogb_or_min(mb);
+  }
+  if (hq >= 0x00100000u) {
+    Eq = static_cast<int>(hq >> 20) - 1023;
+  } else {
+    uint64_t mb = 0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) mb = absmax_bits(xq[j], mb);
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) mb = absmax_bits(sQ(j), mb);
+    Eq = ilogb_or_min(mb);
+  }
   tree_max2i<T, CL>(Ep, Eq, rs_e);
-  // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform)
-  double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
-  double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
+  // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform; the
+  // two-multiply case 2^-E < 2^-1074 is a uniform branch).  Zero padding adds
+  // exact zeros to a non-negative sum.
+  double sp = 0.0, sq = 0.0;
+  if (Ep != kIntMin) {
+    if (-Ep > 1023) {
+      const double a = 0x1p1023, b = pow2i(-Ep - 1023);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) sp = ssq_acc(scale2(xp[j], a, b), sp);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) sp = ssq_acc(scale2(sP(j), a, b), sp);
+    } else {
+      const double a = pow2_any(-Ep);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) sp = ssq_acc(scale1(xp[j], a), sp);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) sp = ssq_acc(scale1(sP(j), a), sp);
+    }
+  }
+  if (Eq != kIntMin) {
+    if (-Eq > 1023) {
+      const double a = 0x1p1023, b = pow2i(-Eq - 1023);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) sq = ssq_acc(scale2(xq[j], a, b), sq);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) sq = ssq_acc(scale2(sQ(j), a, b), sq);
+    } else {
+      const double a = pow2_any(-Eq);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) sq = ssq_acc(scale1(xq[j], a), sq);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) sq = ssq_acc(scale1(sQ(j), a), sq);
+    }
+  }
   tree_sum2<T, CL>(sp, sq, rs_ssq);
   double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
   if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
@@ -108,8 +203,23 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   double zr = 0.0, zi = 0.0;
   const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19 (cluster-uniform)
   if (!zero_col) {
-    double ar, ai;
-    dot_lane<NR>(xq, xp, static_cast<int>(eq), static_cast<int>(ep), ar, ai);
+    const int iq = static_cast<int>(eq), ip = static_cast<int>(ep);
+    double ar = 0.0, ai = 0.0;
+    if (-iq > 1023 || -ip > 1023) {
+      const Pow2 fQ(-iq), fP(-ip);
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        dot_acc(scale2(xq[j], fQ.a, fQ.b), scale2(xp[j], fP.a, fP.b), ar, ai);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j)
+        dot_acc(scale2(sQ(j), fQ.a, fQ.b), scale2(sP(j), fP.a, fP.b), ar, ai);
+    } else {
+      const double aq = pow2_any(-iq), ap = pow2_any(-ip);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) dot_acc(scale1(sQ(j), aq), scale1(sP(j), ap), ar, ai);
+    }
     tree_sum2<T, CL>(ar, ai, rs_dot);
     const Divisor d = make_divisor_normal(fq * fp);  // in [1, 4)
     zr = divide_sf<true, false>(ar, d, kFull);
@@ -117,7 +227,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   }
   // the last read of a peer CTA's shared memory is done: arrive now, wait at
   // exit (the wait keeps this CTA's slots alive for its peers)
-  if constexpr (CL > 1) __cluster_barrier_arrive();
+  if constexpr (CL > 1) {
+    if (!zero_col) __cluster_barrier_arrive();
+  }
   // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
   const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
   const bool transform = P.tol <= az;
@@ -152,9 +264,16 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
     __syncthreads();
     const double c = rot[0], C = rot[1], S = rot[2];
-    // ---- star: rotate the register-resident pair
+    // ---- star: rotate the pair (registers; shared rows back in place)
 #pragma unroll
     for (int j = 0; j < NR; ++j) rot_elem(xp[j], xq[j], c, C, S);
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      E a = sP(j), b = sQ(j);
+      rot_elem(a, b, c, C, S);
+      sP(j) = a;
+      sQ(j) = b;
+    }
   }
   if (transform || sn != 0) {
 #pragma unroll
@@ -163,6 +282,14 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       if (i < P.m) {
         gp[i] = xp[j];
         gq[i] = xq[j];
+      }
+    }
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      const int64_t i = static_cast<int64_t>(NR + j) * W + L;
+      if (i < P.m) {
+        gp[i] = sP(j);
+        gq[i] = sQ(j);
       }
     }
   }
@@ -201,11 +328,18 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
         hm = hi_max(xp[j], hm);
         hm = hi_max(xq[j], hm);
       }
+#pragma unroll 2
+      for (int j = 0; j < NS; ++j) {
+        hm = hi_max(sP(j), hm);
+        hm = hi_max(sQ(j), hm);
+      }
       const uint32_t H = cta_max_u32<T>(hm, rs_m);
       if (hm == H && H != 0u) {
         uint32_t lmax = 0;
 #pragma unroll
         for (int j = 0; j < NR; ++j) lmax = lo_max_at(xp[j], H, lo_max_at(xq[j], H, lmax));
+#pragma unroll 2
+        for (int j = 0; j < NS; ++j) lmax = lo_max_at(sP(j), H, lo_max_at(sQ(j), H, lmax));
         const unsigned long long Mx = (static_cast<unsigned long long>(H) << 32) | lmax;
         atomicMax(P.Mt ? &P.Mt[(P.slot + 1) % 3] : P.mmax, Mx);
       }
@@ -270,26 +404,38 @@ __global__ void __launch_bounds__(T) colnorm_kernel(int64_t m, const double* G, 
 
 // ---- geometry --------------------------------------------------------------
 struct Geo {
-  int T, CL, NR;
+  int T, CL, NR, NS;
 };
 
 // W = 256 * CL lanes (CL = 1 ... 16 CTAs of 256 threads), the smallest W with
-// W * NR >= m.  256-thread CTAs at <= 128 registers leave room for two CTAs
-// (of different pairs) per SM, so one pair's loads overlap another's
-// reductions and EVD.  CL = 16 is a non-portable cluster size (opt-in below).
+// W * NR >= m (NR register rows per lane and column).  256-thread CTAs at
+// <= 128 registers leave room for two CTAs (of different pairs) per SM, so
+// one pair's loads overlap another's reductions and EVD.  Columns that would
+// need W > 2048 hold 2 NR rows per lane instead, NR/2 in registers and 3NR/2
+// in shared memory (96 KB per CTA): W halves, a pair needs half the CTAs,
+// twice as many pairs are in flight.  CL = 16 is a non-portable cluster size (opted in at launch).
 static Geo pick_geo(bool cplx, int64_t m) {
-  const int NR = cplx ? 8 : 16;  // register-resident elements per lane and column
+  const int NR = cplx ? 8 : 16;
   int64_t need = (m + NR - 1) / NR, W = 256;
   while (W < need) W *= 2;
-  if (W > 4096) return Geo{0, 0, 0};
-  return Geo{256, static_cast<int>(W / 256), NR};
+  int NS = 0;
+  if (W > 2048) {
+    NS = NR;
+    need = (m + 2 * NR - 1) / (2 * NR);
+    W = 256;
+    while (W < need) W *= 2;
+  }
+  if (W > 4096) return Geo{0, 0, 0, 0};
+  return Geo{256, static_cast<int>(W / 256), NR, NS};
 }
 
 template <typename Kern, typename... Args>
-static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, cudaStream_t st, Args... args) {
+static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, cudaStream_t st,
+                             Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -302,6 +448,11 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, cudaStream_t s
     cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (a != cudaSuccess) return a;
   }
+  if (smem > 48 * 1024) {
+    cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (a != cudaSuccess) return a;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
   note_launch();
   return e;
@@ -311,13 +462,24 @@ template <bool CPLX>
 static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams& P,
                                  cudaStream_t st) {
   constexpr int NR = CPLX ? 8 : 16;
+  using E = typename Elem<CPLX>::T;
   const int64_t grid = npairs * g.CL;
+  // shared-row geometry: NR/2 rows in registers, 3NR/2 in shared memory
+  // (96 KB per CTA, two CTAs per SM) -- 2 NR rows per lane in all
+  constexpr int NRr = NR / 2, NSs = 3 * NR / 2;
+  const size_t sm = static_cast<size_t>(NSs) * 2 * 256 * sizeof(E);
+  if (g.NS) {
+    switch (g.CL) {
+      case 8: return launch_cl(step_kernel<CPLX, 256, 8, NRr, NSs>, grid, 256, 8, sm, st, P);
+      case 16: return launch_cl(step_kernel<CPLX, 256, 16, NRr, NSs>, grid, 256, 16, sm, st, P);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (g.CL) {
-    case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, P);
-    case 2: return launch_cl(step_kernel<CPLX, 256, 2, NR>, grid, 256, 2, st, P);
-    case 4: return launch_cl(step_kernel<CPLX, 256, 4, NR>, grid, 256, 4, st, P);
-    case 8: return launch_cl(step_kernel<CPLX, 256, 8, NR>, grid, 256, 8, st, P);
-    case 16: return launch_cl(step_kernel<CPLX, 256, 16, NR>, grid, 256, 16, st, P);
+    case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR, 0>, grid, 256, 1, 0, st, P);
+    case 2: return launch_cl(step_kernel<CPLX, 256, 2, NR, 0>, grid, 256, 2, 0, st, P);
+    case 4: return launch_cl(step_kernel<CPLX, 256, 4, NR, 0>, grid, 256, 4, 0, st, P);
+    case 8: return launch_cl(step_kernel<CPLX, 256, 8, NR, 0>, grid, 256, 8, 0, st, P);
   }
   return cudaErrorInvalidValue;
 }
@@ -327,17 +489,25 @@ cudaError_t launch_step(bool cplx, int64_t npairs, const StepParams& P, cudaStre
   return cplx ? launch_step_t<true>(g, npairs, P, st) : launch_step_t<false>(g, npairs, P, st);
 }
 
+// the finalize norms: one column per CTA / cluster, NR + NS rows per lane in
+// registers -- the same W and lane order as the step (R#23)
 template <bool CPLX>
 static cudaError_t launch_colnorm_t(const Geo& g, int64_t m, int64_t n, const double* G,
                                     int64_t ldg, double* ce, double* cf, cudaStream_t st) {
   constexpr int NR = CPLX ? 8 : 16;
   const int64_t grid = n * g.CL;
+  if (g.NS) {
+    switch (g.CL) {
+      case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, 2 * NR>, grid, 256, 8, 0, st, m, G, ldg, ce, cf);
+      case 16: return launch_cl(colnorm_kernel<CPLX, 256, 16, 2 * NR>, grid, 256, 16, 0, st, m, G, ldg, ce, cf);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (g.CL) {
-    case 1: return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, st, m, G, ldg, ce, cf);
-    case 2: return launch_cl(colnorm_kernel<CPLX, 256, 2, NR>, grid, 256, 2, st, m, G, ldg, ce, cf);
-    case 4: return launch_cl(colnorm_kernel<CPLX, 256, 4, NR>, grid, 256, 4, st, m, G, ldg, ce, cf);
-    case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, NR>, grid, 256, 8, st, m, G, ldg, ce, cf);
-    case 16: return launch_cl(colnorm_kernel<CPLX, 256, 16, NR>, grid, 256, 16, st, m, G, ldg, ce, cf);
+    case 1: return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, 0, st, m, G, ldg, ce, cf);
+    case 2: return launch_cl(colnorm_kernel<CPLX, 256, 2, NR>, grid, 256, 2, 0, st, m, G, ldg, ce, cf);
+    case 4: return launch_cl(colnorm_kernel<CPLX, 256, 4, NR>, grid, 256, 4, 0, st, m, G, ldg, ce, cf);
+    case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, NR>, grid, 256, 8, 0, st, m, G, ldg, ce, cf);
   }
   return cudaErrorInvalidValue;
 }
