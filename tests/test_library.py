@@ -79,10 +79,10 @@ def test_gpu_calls_fail_loudly_without_cuda():
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("m", [1, 64, 256, 4096, 8192, 32768, 65536])
+@pytest.mark.parametrize("m", [1, 64, 256, 4096, 8192, 32768, 65536, 131072])
 def test_step_rspec_is_a_valid_reduction_spec(cplx, m):
     import paper_2202_08361_b200 as J
-    if cplx and m > 32768:
+    if cplx and m > 65536:
         with pytest.raises(J.JsvdError):
             J.step_rspec(cplx, m)
         return
@@ -90,5 +90,6 @@ def test_step_rspec_is_a_valid_reduction_spec(cplx, m):
     assert c == 1 and W >= 256 and W & (W - 1) == 0
     assert sorted(offs) == [1 << k for k in range(W.bit_length() - 1)]
     assert offs[:5] == (16, 8, 4, 2, 1)
-    per_lane = -(-m // W)
-    assert per_lane <= (8 if cplx else 16)
+    per_lane = -(-m // W)  # register rows, plus as many shared-memory rows past W = 2048
+    assert per_lane <= (16 if cplx else 32)
+    assert W <= 2048 or per_lane > (8 if cplx else 16) or m <= W * (8 if cplx else 16)
