@@ -250,15 +250,15 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           const double ep = zp ? -INFINITY : static_cast<double>(s0.ep);
           const double eq = zq ? -INFINITY : static_cast<double>(s0.eq);
           // z = (ar, ai) / fl(fq fp), fl(fq fp) in [1, 4) (Alg 3.1 line 8)
-          const Divisor d = make_divisor_normal(fq * fp);
-          const double zr = divide_sf<true, false>(s0.ar, d, kFull);
-          const double zi = CPLX ? divide_sf<true, false>(s0.ai, d, kFull) : 0.0;
+          const Rcp d = rcp_plain(fq * fp);
+          const double zr = dot_div(s0.ar, d, kFull);
+          const double zi = CPLX ? dot_div(s0.ai, d, kFull) : 0.0;
           const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
           const bool tr = act && !(zp || zq) && tol <= az;  // Alg 3.2
           if (__any_sync(kFull, tr)) {
             double b11, b22, br, bi;
-            gram(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
-                 tr ? fq : 1.0, b11, b22, br, bi);
+            gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
+                      tr ? fq : 1.0, b11, b22, br, bi, kFull);
             const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);
             if (tr) {
               slots[l].c = o.c;

@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       for (int j = 0; j < NS; ++j) dot_acc(scale1(sQ(j), aq), scale1(sP(j), ap), ar, ai);
     }
     tree_sum2<T, CL>(ar, ai, rs_dot);
-    const Divisor d = make_divisor_normal(fq * fp);  // in [1, 4)
-    zr = divide_sf<true, false>(ar, d, kFull);
-    zi = CPLX ? divide_sf<true, false>(ai, d, kFull) : 0.0;
+    const Rcp d = rcp_plain(fq * fp);  // fl(f_q f_p) in [1, 4)
+    zr = dot_div(ar, d, kFull);
+    zi = CPLX ? dot_div(ai, d, kFull) : 0.0;
   }
   // the last read of a peer CTA's shared memory is done: arrive now, wait at
   // exit (the wait keeps this CTA's slots alive for its peers)
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   if (transform) {
     if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
       double b11, b22, br, bi;
-      gram(zr, zi, ep, fp, eq, fq, b11, b22, br, bi);
+      gram_fast(zr, zi, ep, fp, eq, fq, b11, b22, br, bi, kFull);
       const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);  // warp 0, all lanes
       if (threadIdx.x == 0) {
         rot[0] = o.c;

@@ -326,6 +326,54 @@ __device__ __forceinline__ void gram(double zr, double zi, double e1, double f1,
   bi = scalbn_rn(zi, static_cast<int>(sA));
 }
 
+// Alg 3.3 for the norm significands the step produces (f1, f2 in [1, 2), e
+// integral): f12 = f1/f2 and f21 = f2/f1 lie in (1/2, 2), so both quotients
+// are plain divisions, logb is -1 or 0 and getmant a doubling.  The common
+// case -- s_A = 0 and both exponents >= -1022 -- then needs one exact multiply
+// per diagonal entry and leaves z unscaled; any lane outside it (exponents of
+// the two norms more than ~1022 apart) takes gram() in a uniform branch.
+// Same bits as gram() for every input it accepts (tested against the oracle).
+__device__ __forceinline__ void gram_fast(double zr, double zi, double e1, double f1, double e2,
+                                          double f2, double& a11, double& a22, double& br,
+                                          double& bi, unsigned mask) {
+  double f12 = div_plain(f1, rcp_plain(f2));
+  double f21 = div_plain(f2, rcp_plain(f1));
+  int e12 = static_cast<int>(e1 - e2), e21 = -e12;
+  const bool l12 = f12 < 1.0, l21 = f21 < 1.0;
+  e12 -= l12 ? 1 : 0;
+  e21 -= l21 ? 1 : 0;
+  f12 = l12 ? f12 * 2.0 : f12;
+  f21 = l21 ? f21 * 2.0 : f21;
+  const bool fast = max(e12, e21) <= kEtaHat && min(e12, e21) >= -1022;
+  a11 = f12 * pow2i(fast ? e12 : 0);
+  a22 = f21 * pow2i(fast ? e21 : 0);
+  br = zr;
+  bi = zi;
+  if (__any_sync(mask, !fast)) {
+    double g11, g22, gr, gi;
+    gram(zr, zi, e1, f1, e2, f2, g11, g22, gr, gi);
+    if (!fast) {
+      a11 = g11;
+      a22 = g22;
+      br = gr;
+      bi = gi;
+    }
+  }
+}
+
+// z = a / d for the dot's sums over d = fl(f_q f_p) in [1, 4) (Alg 3.1 line
+// 8): the plain division when |a| >= 2^-968 (then the quotient is normal),
+// the general one in a uniform branch for tiny or zero sums
+__device__ __forceinline__ double dot_div(double a, const Rcp& r, unsigned mask) {
+  double z = div_plain(a, r);
+  const bool tiny = !(fabs(a) >= 0x1p-968);
+  if (__any_sync(mask, tiny)) {
+    const double g = divide_sf<true, false>(a, make_divisor_normal(r.d), mask);
+    z = tiny ? g : z;
+  }
+  return z;
+}
+
 // ---------------------------------------------------------------- strategy
 // R#20: circle method on P players, round r: position 0 = player 0, position
 // k >= 1 = player ((k-1+r) mod (P-1)) + 1; pair i = positions (i, P-1-i).
