@@ -22,55 +22,79 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
   return x;
 }
 
+// streaming loads of one chunk (512 matrices per CTA, 2 per thread); lanes
+// past r read zeros (every lane runs the EVD so the rare-case votes can use
+// the full warp mask)
+template <bool CPLX>
+struct Chunk2 {
+  double2 a11, a22, re, im;
+  __device__ __forceinline__ void load(int64_t r, int64_t tid, const double* __restrict__ p11,
+                                       const double* __restrict__ p22,
+                                       const double* __restrict__ pre,
+                                       const double* __restrict__ pim) {
+    const int64_t l0 = 2 * tid;
+    a11 = a22 = re = im = make_double2(0.0, 0.0);
+    if (l0 + 1 < r) {
+      a11 = __ldcs(reinterpret_cast<const double2*>(p11) + tid);
+      a22 = __ldcs(reinterpret_cast<const double2*>(p22) + tid);
+      re = __ldcs(reinterpret_cast<const double2*>(pre) + tid);
+      if (CPLX) im = __ldcs(reinterpret_cast<const double2*>(pim) + tid);
+    } else if (l0 < r) {  // ragged tail: one matrix
+      a11.x = p11[l0];
+      a22.x = p22[l0];
+      re.x = pre[l0];
+      if (CPLX) im.x = pim[l0];
+    }
+  }
+};
+
+// Persistent streaming kernel: each CTA walks chunks c = blockIdx.x,
+// blockIdx.x + gridDim.x, ... and loads chunk c + gridDim.x before computing
+// chunk c, so the HBM latency of the next loads overlaps this chunk's EVDs;
+// the grid is sized to the resident CTAs (no tail wave).
 template <bool CPLX, bool TAN, bool NOBACK>
-__global__ void __launch_bounds__(256) evd2_vec2_kernel(
+__global__ void __launch_bounds__(256, 3) evd2_vec2_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t l0 = 2 * tid;
-  // every lane runs the EVD (zeros past the tail) so the rare-case votes can
-  // use the full warp mask
-  double2 x11 = make_double2(0.0, 0.0), x22 = x11, xre = x11, xim = x11;
-  if (l0 + 1 < r) {
-    x11 = __ldcs(reinterpret_cast<const double2*>(a11) + tid);
-    x22 = __ldcs(reinterpret_cast<const double2*>(a22) + tid);
-    xre = __ldcs(reinterpret_cast<const double2*>(are) + tid);
-    if (CPLX) xim = __ldcs(reinterpret_cast<const double2*>(aim) + tid);
-  } else if (l0 < r) {  // ragged tail: one matrix
-    x11.x = a11[l0];
-    x22.x = a22[l0];
-    xre.x = are[l0];
-    if (CPLX) xim.x = aim[l0];
-  }
-  const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x11.x, x22.x, xre.x, xim.x, kFull);
-  const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x11.y, x22.y, xre.y, xim.y, kFull);
-  const bool p0 = l0 < r && e0.perm, p1 = l0 + 1 < r && e1.perm;
-  if (l0 + 1 < r) {
-    __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
-    __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
-    __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
-    __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
-    if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
-    if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
-  } else if (l0 < r) {
-    l1[l0] = e0.l1;
-    l2[l0] = e0.l2;
-    cs[l0] = e0.c;
-    sr[l0] = e0.sr;
-    if (CPLX) si[l0] = e0.si;
-    if (zeta) zeta[l0] = e0.zeta;
-  }
-  if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
-    const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
-    const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
-    const int lane = threadIdx.x & 31;
-    const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
-    const int64_t nwords = (r + 31) / 32;
-    if (lane < 2 && wbase + lane < nwords) {
-      const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
-      perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
+  const int64_t nchunks = (r + 511) / 512;
+  int64_t c = blockIdx.x;
+  Chunk2<CPLX> nx;
+  if (c < nchunks) nx.load(r, c * 256 + threadIdx.x, a11, a22, are, aim);
+  for (; c < nchunks; c += gridDim.x) {
+    const Chunk2<CPLX> x = nx;
+    const int64_t tid = c * 256 + threadIdx.x;
+    const int64_t l0 = 2 * tid;
+    if (c + gridDim.x < nchunks) nx.load(r, (c + gridDim.x) * 256 + threadIdx.x, a11, a22, are, aim);
+    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x.a11.x, x.a22.x, x.re.x, x.im.x, kFull);
+    const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x.a11.y, x.a22.y, x.re.y, x.im.y, kFull);
+    const bool p0 = l0 < r && e0.perm, p1 = l0 + 1 < r && e1.perm;
+    if (l0 + 1 < r) {
+      __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
+      __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
+      __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
+      __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
+      if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
+      if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
+    } else if (l0 < r) {
+      l1[l0] = e0.l1;
+      l2[l0] = e0.l2;
+      cs[l0] = e0.c;
+      sr[l0] = e0.sr;
+      if (CPLX) si[l0] = e0.si;
+      if (zeta) zeta[l0] = e0.zeta;
+    }
+    if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
+      const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
+      const int lane = threadIdx.x & 31;
+      const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
+      const int64_t nwords = (r + 31) / 32;
+      if (lane < 2 && wbase + lane < nwords) {
+        const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
+        perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
+      }
     }
   }
 }
@@ -108,7 +132,18 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
                                cudaStream_t st) {
   const int threads = 256;
   if (vec) {
-    const int64_t blocks = (r + 2 * threads - 1) / (2 * threads);
+    // one CTA per resident slot (queried once per instantiation)
+    static int slots = 0;
+    if (!slots) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, evd2_vec2_kernel<CPLX, TAN, NOBACK>,
+                                                    threads, 0);
+      slots = sms * (per > 0 ? per : 1);
+    }
+    const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
+    const int64_t blocks = chunks < slots ? chunks : slots;
     evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
         r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
   } else {
