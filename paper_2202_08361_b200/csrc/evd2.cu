@@ -48,55 +48,72 @@ struct Chunk2 {
   }
 };
 
-// Persistent streaming kernel: each CTA walks chunks c = blockIdx.x,
-// blockIdx.x + gridDim.x, ... and loads chunk c + gridDim.x before computing
-// chunk c, so the HBM latency of the next loads overlaps this chunk's EVDs;
-// the grid is sized to the resident CTAs (no tail wave).
+// one chunk: 512 consecutive matrices, 2 per thread (LDG.128 / STG.128 of
+// every SoA stream); the permutation words from two warp ballots
 template <bool CPLX, bool TAN, bool NOBACK>
-__global__ void __launch_bounds__(256, 3) evd2_vec2_kernel(
+__device__ __forceinline__ void evd2_chunk(
+    int64_t c, int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
+    const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
+    double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+  const int64_t tid = c * 256 + threadIdx.x;
+  const int64_t l0 = 2 * tid;
+  Chunk2<CPLX> x;
+  x.load(r, tid, a11, a22, are, aim);
+  const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x.a11.x, x.a22.x, x.re.x, x.im.x, kFull);
+  const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x.a11.y, x.a22.y, x.re.y, x.im.y, kFull);
+  const bool p0 = l0 < r && e0.perm, p1 = l0 + 1 < r && e1.perm;
+  if (l0 + 1 < r) {
+    __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
+    __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
+    __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
+    __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
+    if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
+    if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
+  } else if (l0 < r) {
+    l1[l0] = e0.l1;
+    l2[l0] = e0.l2;
+    cs[l0] = e0.c;
+    sr[l0] = e0.sr;
+    if (CPLX) si[l0] = e0.si;
+    if (zeta) zeta[l0] = e0.zeta;
+  }
+  if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
+    const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
+    const int64_t nwords = (r + 31) / 32;
+    if (lane < 2 && wbase + lane < nwords) {
+      const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
+      perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
+    }
+  }
+}
+
+// one chunk per CTA (r/512 CTAs: the large batches, configs[1])
+template <bool CPLX, bool TAN, bool NOBACK>
+__global__ void __launch_bounds__(256) evd2_vec2_kernel(
+    int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
+    const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
+    double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+  evd2_chunk<CPLX, TAN, NOBACK>(blockIdx.x, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
+}
+
+// Persistent variant for small batches (configs[0]: 2048 chunks = 3.5 waves of
+// one-chunk CTAs): each CTA walks chunks c = blockIdx.x, blockIdx.x +
+// gridDim.x, ...; the grid is sized to the resident CTAs, so there is no
+// partial last wave (every SM gets the same number of chunks to within one).
+template <bool CPLX, bool TAN, bool NOBACK>
+__global__ void __launch_bounds__(256, 4) evd2_persist_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
   const int64_t nchunks = (r + 511) / 512;
-  int64_t c = blockIdx.x;
-  Chunk2<CPLX> nx;
-  if (c < nchunks) nx.load(r, c * 256 + threadIdx.x, a11, a22, are, aim);
-  for (; c < nchunks; c += gridDim.x) {
-    const Chunk2<CPLX> x = nx;
-    const int64_t tid = c * 256 + threadIdx.x;
-    const int64_t l0 = 2 * tid;
-    if (c + gridDim.x < nchunks) nx.load(r, (c + gridDim.x) * 256 + threadIdx.x, a11, a22, are, aim);
-    const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x.a11.x, x.a22.x, x.re.x, x.im.x, kFull);
-    const Evd2Out e1 = evd2<CPLX, TAN, NOBACK>(x.a11.y, x.a22.y, x.re.y, x.im.y, kFull);
-    const bool p0 = l0 < r && e0.perm, p1 = l0 + 1 < r && e1.perm;
-    if (l0 + 1 < r) {
-      __stcs(reinterpret_cast<double2*>(l1) + tid, make_double2(e0.l1, e1.l1));
-      __stcs(reinterpret_cast<double2*>(l2) + tid, make_double2(e0.l2, e1.l2));
-      __stcs(reinterpret_cast<double2*>(cs) + tid, make_double2(e0.c, e1.c));
-      __stcs(reinterpret_cast<double2*>(sr) + tid, make_double2(e0.sr, e1.sr));
-      if (CPLX) __stcs(reinterpret_cast<double2*>(si) + tid, make_double2(e0.si, e1.si));
-      if (zeta) __stcs(reinterpret_cast<int2*>(zeta) + tid, make_int2(e0.zeta, e1.zeta));
-    } else if (l0 < r) {
-      l1[l0] = e0.l1;
-      l2[l0] = e0.l2;
-      cs[l0] = e0.c;
-      sr[l0] = e0.sr;
-      if (CPLX) si[l0] = e0.si;
-      if (zeta) zeta[l0] = e0.zeta;
-    }
-    if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
-      const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
-      const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
-      const int lane = threadIdx.x & 31;
-      const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
-      const int64_t nwords = (r + 31) / 32;
-      if (lane < 2 && wbase + lane < nwords) {
-        const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
-        perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
-      }
-    }
-  }
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
+    evd2_chunk<CPLX, TAN, NOBACK>(c, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
 }
 
 // scalar path for pointers that are only 8-byte aligned
@@ -138,14 +155,19 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
       int dev = 0, sms = 0, per = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, evd2_vec2_kernel<CPLX, TAN, NOBACK>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, evd2_persist_kernel<CPLX, TAN, NOBACK>,
                                                     threads, 0);
       slots = sms * (per > 0 ? per : 1);
     }
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
-    const int64_t blocks = chunks < slots ? chunks : slots;
-    evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+    if (chunks <= 64 * static_cast<int64_t>(slots)) {  // a few waves: tail effects matter
+      const int64_t blocks = chunks < slots ? chunks : slots;
+      evd2_persist_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+    } else {
+      evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
+          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+    }
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
