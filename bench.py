@@ -114,6 +114,7 @@ def _ncores():
 # --------------------------------------------------------------- workloads
 class EvdWorkload:
     """configs[0] / configs[1]: batched 2x2 EVD (jsvd_evd2_batched)."""
+    graphable = True
 
     def __init__(self, name, rank, world):
         import torch
@@ -202,6 +203,7 @@ class StepWorkload:
     """configs[2]: one parallel Jacobi step (jsvd_sweep_step) of the 4096 x 1024
     real SVD, steps 0.. of the first sweep (every pair transformed), G and V as
     jsvd_gesvj leaves them after its initial scaling (Eq. skn) and V = I."""
+    graphable = True
 
     def __init__(self, name, rank, world):
         import torch
@@ -618,13 +620,36 @@ def run_jsvd(args):
     if hasattr(wl, "skip_to"):  # dist: let the timed window straddle a block exchange
         wl.skip_to(max(wl.k, 2 * wl.S.b - 1 - args.steps // 2))
         torch.cuda.synchronize()
+    # steps that are pure asynchronous launches (no host sync, no per-step
+    # preparation) are captured once as a CUDA graph of exactly K steps and
+    # timed as one replay: the device time of the K launches without the
+    # Python/ctypes enqueue cost between them
+    graph = None
+    if getattr(wl, "graphable", False) and world == 1 and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        nc0 = J.launch_count()
+        with torch.cuda.graph(graph):
+            cap = torch.cuda.current_stream()
+            for _ in range(args.steps):
+                wl.step(cap)
+        graph_launches = J.launch_count() - nc0
+        torch.cuda.synchronize()
+        if hasattr(wl, "reset_counters"):
+            wl.reset_counters()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     n0 = J.launch_count()
     evs = []
     with ClockSampler(local) as clk:
-        if per_step_events:  # preparation (L2 flush / input restore) outside the timing
+        if graph is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+        elif per_step_events:  # preparation (L2 flush / input restore) outside the timing
             for _ in range(args.steps):
                 wl.prepare()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -643,6 +668,8 @@ def run_jsvd(args):
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
     launches = J.launch_count() - n0
+    if graph is not None:
+        launches = graph_launches  # the replay launches exactly the captured kernels
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -718,6 +745,9 @@ def run_jsvd(args):
             "dtype": "f64",
             "data": "synthetic (counter-based SplitMix64, DESIGN.md recipe)",
             "config": {"workload": wl.desc, "units_per_gpu_step": wl.units_per_step,
+                       "timing": ("one CUDA-graph replay of the K steps (CUDA events)" if graph is not None
+                                  else "per-step CUDA events" if per_step_events else
+                                  "CUDA events around K launches"),
                        "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
                        "l2": wl.l2_note},
             "e2e": {"value": e2e_val, "unit": wl.unit, "h2d_bytes_per_step": h2d,
@@ -803,6 +833,8 @@ def main():
     ap.add_argument("--impl", default="jsvd", choices=["jsvd", "reference"])
     ap.add_argument("--workload", default="evd_c64", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the K steps as individual launches instead of one CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:

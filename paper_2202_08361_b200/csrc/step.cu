@@ -13,6 +13,9 @@
 //   star   rotation of g_p, g_q in registers + store, then v_p, v_q (Alg 3.4)
 // so G is read once and written once per transformed pair, V read+written
 // once per transformed pair, nothing for a converged pair (R#26: no max on V).
+#include <mutex>
+#include <vector>
+
 #include "jsvd_host.h"
 #include "step_dev.cuh"
 #include "step_params.h"
@@ -429,6 +432,19 @@ static Geo pick_geo(bool cplx, int64_t m) {
   return Geo{256, static_cast<int>(W / 256), NR, NS};
 }
 
+static std::mutex g_attr_mu;
+static std::vector<const void*> g_attr_done;
+static bool attrs_done(const void* k) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  for (const void* p : g_attr_done)
+    if (p == k) return true;
+  return false;
+}
+static void mark_attrs_done(const void* k) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  g_attr_done.push_back(k);
+}
+
 template <typename Kern, typename... Args>
 static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, cudaStream_t st,
                              Args... args) {
@@ -444,14 +460,19 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CL > 1 ? 1 : 0;
-  if (CL > 8) {
-    cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (a != cudaSuccess) return a;
-  }
-  if (smem > 48 * 1024) {
-    cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (a != cudaSuccess) return a;
+  // kernel attributes are set once per kernel (not inside a CUDA-graph capture
+  // of later launches)
+  if ((CL > 8 || smem > 48 * 1024) && !attrs_done(reinterpret_cast<const void*>(k))) {
+    if (CL > 8) {
+      cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (a != cudaSuccess) return a;
+    }
+    if (smem > 48 * 1024) {
+      cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (a != cudaSuccess) return a;
+    }
+    mark_attrs_done(reinterpret_cast<const void*>(k));
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
   note_launch();
