@@ -66,7 +66,7 @@ def _scaled_input(rng, m, n, cplx, specials=True):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("m", [1, 7, 64, 255, 256, 257, 1000, 2049, 4096, 8191, 16384, 32768])
+@pytest.mark.parametrize("m", [1, 7, 64, 255, 256, 257, 1000, 2049, 4096, 8191, 16384, 20001, 32768])
 def test_sweep_step_bitwise(J, cplx, m):
     if not cplx and m == 32768:
         m = 65536  # the real 8-CTA cluster geometry
