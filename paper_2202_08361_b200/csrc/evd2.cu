@@ -7,6 +7,8 @@
 // one 16-byte STG.128; the permutation words are assembled from two
 // warp ballots.  No shared memory, no synchronisation.  Grid: one 256-thread
 // CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110 waves at 8 CTAs/SM).
+#include <cstdlib>
+
 #include "jsvd_dev.cuh"
 #include "jsvd_host.h"
 
@@ -160,7 +162,13 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
       slots = sms * (per > 0 ? per : 1);
     }
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
-    if (chunks <= 64 * static_cast<int64_t>(slots)) {  // a few waves: tail effects matter
+    static const int persist_mode = [] {  // JSVD_EVD_PERSIST=0/1 forces a variant (A/B timing)
+      const char* e = getenv("JSVD_EVD_PERSIST");
+      return e ? atoi(e) : -1;
+    }();
+    const bool persist = persist_mode >= 0 ? persist_mode == 1
+                                           : chunks <= 64 * static_cast<int64_t>(slots);
+    if (persist) {  // a few waves: tail effects matter
       const int64_t blocks = chunks < slots ? chunks : slots;
       evd2_persist_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
           r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
