@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* sG = reinterpret_cast<E*>(smem_raw);
   E* sV = sG + m * n;
-  PairSlot* slots = reinterpret_cast<PairSlot*>(sV + n * n);
-  double* ce = reinterpret_cast<double*>(slots + n / 2);
+  PairSlot* slots2 = reinterpret_cast<PairSlot*>(sV + n * n);  // [2][n/2]: steps alternate
+  double* ce = reinterpret_cast<double*>(slots2 + n);
   double* cf = ce + n;
   uint8_t* sPairs = reinterpret_cast<uint8_t*>(cf + n);  // (n-1) x n/2 pivot pairs (n <= 64)
   __shared__ unsigned long long sM0;
@@ -173,12 +173,34 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   if (threadIdx.x == 0) sMt = hi32(scalbn_rn(M0, s));
   __syncthreads();
 
+  // V of step k is rotated by warps 1..7 while warp 0 runs phase B of step
+  // k+1 (V never enters a decision, Alg 3.4 applies the same (c, C, S) to it);
+  // the slots of consecutive steps alternate between two buffers
+  const auto rotate_v = [&](const PairSlot* sl_, int kstep, int l_begin, int l_step, int lane0,
+                            int lanes) {
+    for (int l = l_begin; l < np; l += l_step) {
+      const PairSlot& sl = sl_[l];
+      if (!sl.transform) continue;
+      const int p = sPairs[2 * (kstep * np + l)], q = sPairs[2 * (kstep * np + l) + 1];
+      E* vp = sV + p * ni;
+      E* vq = sV + q * ni;
+      for (int i = lane0; i < ni; i += lanes) {
+        E a = vp[i], bq = vq[i];
+        rot_elem(a, bq, sl.c, sl.C, sl.S);
+        vp[i] = a;
+        vq[i] = bq;
+      }
+    }
+  };
+  int pend_k = -1, pend_buf = 0;  // step whose V rotation is pending
+  int gstep = 0;
   int C = 0;
   int64_t Ttot = 0;  // transformed pair-steps (thread 0)
   bool converged = false;
   for (C = 0; C < max_sweeps; ++C) {
     if (threadIdx.x == 0) sT = 0;
-    for (int k = 0; k < ni - 1; ++k) {
+    for (int k = 0; k < ni - 1; ++k, ++gstep) {
+      PairSlot* slots = slots2 + (gstep & 1) * np;
       // ---- line 6: rescale check (every step for flat round-robin); M-tilde
       // is normal here (G is scaled to ~ omega / m), so its high word's
       // exponent field is floor(lg M-tilde)
@@ -270,9 +292,11 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           tcount += __popc(__ballot_sync(0xffffffffu, tr));
         }
         if (lane == 0) sT += tcount;
+      } else if (pend_k >= 0) {  // half-warps 2..15: V of the previous step
+        rotate_v(slots2 + pend_buf * np, pend_k, hw - 2, kBNH - 2, hl, kBW);
       }
       __syncthreads();
-      // ---- phase C: rotations of G and V (Alg 3.4), M-tilde
+      // ---- phase C: rotations of G (Alg 3.4), M-tilde
       uint32_t Mw = 0;
       for (int l = hw; l < np; l += kBNH) {
         const PairSlot& sl = slots[l];
@@ -300,15 +324,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
             }
           }
         }
-        E* vp = sV + p * ni;
-        E* vq = sV + q * ni;
-        for (int i = hl; i < ni; i += kBW) {
-          E a = vp[i], bq = vq[i];
-          rot_elem(a, bq, c, Cc, S);
-          vp[i] = a;
-          vq[i] = bq;
-        }
       }
+      pend_k = k;
+      pend_buf = gstep & 1;
       Mw = __reduce_max_sync(0xffffffffu, Mw);
       if (lane == 0 && Mw > sMt) atomicMax(&sMt, Mw);
       __syncthreads();
@@ -319,6 +337,10 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       ++C;
       break;
     }
+    __syncthreads();
+  }
+  if (pend_k >= 0) {  // the last step's V rotation
+    rotate_v(slots2 + pend_buf * np, pend_k, hw, kBNH, hl, kBW);
     __syncthreads();
   }
   // ---- finalize: norms with the step's R (R#23),
@@ -397,7 +419,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 
 static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
   const size_t w = cplx ? 16 : 8;
-  return w * (m * n + n * n) + sizeof(PairSlot) * (n / 2) + 2 * sizeof(double) * n +
+  return w * (m * n + n * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
          2 * (n - 1) * (n / 2);
 }
 

@@ -7,8 +7,6 @@
 // one 16-byte STG.128; the permutation words are assembled from two
 // warp ballots.  No shared memory, no synchronisation.  Grid: one 256-thread
 // CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110 waves at 8 CTAs/SM).
-#include <cstdlib>
-
 #include "jsvd_dev.cuh"
 #include "jsvd_host.h"
 
@@ -103,21 +101,6 @@ __global__ void __launch_bounds__(256) evd2_vec2_kernel(
   evd2_chunk<CPLX, TAN, NOBACK>(blockIdx.x, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
 }
 
-// Persistent variant for small batches (configs[0]: 2048 chunks = 3.5 waves of
-// one-chunk CTAs): each CTA walks chunks c = blockIdx.x, blockIdx.x +
-// gridDim.x, ...; the grid is sized to the resident CTAs, so there is no
-// partial last wave (every SM gets the same number of chunks to within one).
-template <bool CPLX, bool TAN, bool NOBACK>
-__global__ void __launch_bounds__(256, 4) evd2_persist_kernel(
-    int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
-    const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
-    double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
-    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
-  const int64_t nchunks = (r + 511) / 512;
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
-    evd2_chunk<CPLX, TAN, NOBACK>(c, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
-}
-
 // scalar path for pointers that are only 8-byte aligned
 template <bool CPLX, bool TAN, bool NOBACK>
 __global__ void __launch_bounds__(256) evd2_scalar_kernel(
@@ -151,31 +134,11 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
                                cudaStream_t st) {
   const int threads = 256;
   if (vec) {
-    // one CTA per resident slot (queried once per instantiation)
-    static int slots = 0;
-    if (!slots) {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, evd2_persist_kernel<CPLX, TAN, NOBACK>,
-                                                    threads, 0);
-      slots = sms * (per > 0 ? per : 1);
-    }
+    // one 512-matrix chunk per CTA: the measured-best shape for both configs
+    // (a persistent grid-stride variant was slower for configs[0] and [1])
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
-    static const int persist_mode = [] {  // JSVD_EVD_PERSIST=0/1 forces a variant (A/B timing)
-      const char* e = getenv("JSVD_EVD_PERSIST");
-      return e ? atoi(e) : -1;
-    }();
-    const bool persist = persist_mode >= 0 ? persist_mode == 1
-                                           : chunks <= 64 * static_cast<int64_t>(slots);
-    if (persist) {  // a few waves: tail effects matter
-      const int64_t blocks = chunks < slots ? chunks : slots;
-      evd2_persist_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
-    } else {
-      evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
-          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
-    }
+    evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
+        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(

@@ -169,7 +169,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
 #pragma unroll 2
       for (int j = 0; j < NS; ++j) sp = ssq_acc(scale2(sP(j), a, b), sp);
     } else {
-      const double a = pow2_any(-Ep);
+      // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
+      // field only; a subnormal 2^-E (outside it) the general construction
+      const double a = -Ep >= -1022 ? pow2i(-Ep) : pow2_any(-Ep);
 #pragma unroll
       for (int j = 0; j < NR; ++j) sp = ssq_acc(scale1(xp[j], a), sp);
 #pragma unroll 2
@@ -184,7 +186,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
 #pragma unroll 2
       for (int j = 0; j < NS; ++j) sq = ssq_acc(scale2(sQ(j), a, b), sq);
     } else {
-      const double a = pow2_any(-Eq);
+      // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
+      // field only; a subnormal 2^-E (outside it) the general construction
+      const double a = -Eq >= -1022 ? pow2i(-Eq) : pow2_any(-Eq);
 #pragma unroll
       for (int j = 0; j < NR; ++j) sq = ssq_acc(scale1(xq[j], a), sq);
 #pragma unroll 2

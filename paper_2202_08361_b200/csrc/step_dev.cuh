@@ -258,8 +258,12 @@ __device__ __forceinline__ double ssq_lane(const E* x, int Ex) {
     const double a = 0x1p1023, b = pow2i(-Ex - 1023);
 #pragma unroll
     for (int j = 0; j < NR; ++j) s = ssq_acc(scale2(x[j], a, b), s);
-  } else {
+  } else if (-Ex < -1022) {  // 2^-E subnormal (max |x| >= 2^1023: outside the step's precondition)
     const double a = pow2_any(-Ex);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s = ssq_acc(scale1(x[j], a), s);
+  } else {  // the common case: 2^-E normal, built from its exponent field alone
+    const double a = pow2i(-Ex);
 #pragma unroll
     for (int j = 0; j < NR; ++j) s = ssq_acc(scale1(x[j], a), s);
   }
@@ -279,8 +283,12 @@ __device__ __forceinline__ void dot_lane(const E* xq, const E* xp, int eq, int e
 #pragma unroll
     for (int j = 0; j < NR; ++j)
       dot_acc(scale2(xq[j], fQ.a, fQ.b), scale2(xp[j], fP.a, fP.b), ar, ai);
-  } else {
+  } else if (-eq < -1022 || -ep < -1022) {
     const double aq = pow2_any(-eq), ap = pow2_any(-ep);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
+  } else {  // the common case: both factors normal powers of two
+    const double aq = pow2i(-eq), ap = pow2i(-ep);
 #pragma unroll
     for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
   }
