@@ -213,6 +213,7 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
       case 5: q[i] = hypot_naive(fabs(x), fabs(y)); break;
       case 7: q[i] = sqrt_plain(x); break;
       case 8: q[i] = div_plain(x, rcp_plain(y)); break;
+      case 9: q[i] = divide_small(x, rcp_plain(y), __activemask()); break;
       default: q[i] = divide_sf<false, true>(x, make_divisor(y), __activemask()); break;
     }
   }
@@ -221,7 +222,7 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
 
 extern "C" jsvd_status jsvd_debug_primitive(int32_t mode, int64_t n, const double* a,
                                             const double* b, double* q, void* stream) {
-  if (n < 0 || mode < 0 || mode > 8) return JSVD_EINVAL;
+  if (n < 0 || mode < 0 || mode > 9) return JSVD_EINVAL;
   if (n == 0) return JSVD_OK;
   jsvd::debug_div_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
                            static_cast<cudaStream_t>(stream)>>>(n, a, b, q, mode);

@@ -176,3 +176,26 @@ def test_div_plain_in_range():
         x, y = np.ldexp(A.ravel(), ea), np.ldexp(B.ravel(), eb)
         bad = _same(_run(8, x, y), x / y)
         assert bad.size == 0, (ea, eb, x[bad[:4]], y[bad[:4]])
+
+
+def test_divide_small_full_dividend_range():
+    # a / d, d in [1, 2], a anywhere (subnormal quotients, exact ties on the
+    # subnormal grid, signed zeros): the EVD's e^{ia} sin(phi) = e^{ia} tan / sec
+    rng = np.random.default_rng(23)
+    n = 1 << 22
+    d = np.concatenate([1 + rng.random(n), np.array([1.0, 2.0, np.sqrt(2.0), 2.0 - 2.0 ** -52])])
+    a = _rand_doubles(rng, d.size)
+    a[::5] = np.ldexp(1 + rng.random(a[::5].size), rng.integers(-1080, -1000, a[::5].size))
+    a[::7] *= -1
+    a[3] = -0.0
+    bad = _same(_run(9, a, d), a / d)
+    assert bad.size == 0, (a[bad[:4]], d[bad[:4]])
+    # exact ties of the final rounding (a = odd 2^-1074, d = 2: a/d is a midpoint
+    # of the subnormal grid; exact ties need d a power of two) and near ties
+    odd = (2 * rng.integers(0, 1 << 51, 1 << 16) + 1).astype(np.float64)
+    x = np.ldexp(odd, -1074)
+    for dv in (2.0, 2.0 - 2.0 ** -52, 1.0 + 2.0 ** -52, 1.0, 1.5, 1.0 + 2.0 ** -26):
+        dd = np.full(x.size, dv)
+        for y in (x, -x):
+            bad = _same(_run(9, y, dd), y / dd)
+            assert bad.size == 0, (dv, y[bad[:4]])
