@@ -99,7 +99,8 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
   e = E + k / 2;
 }
 
-template <bool CPLX, int NR>
+// FULL: m == 16 NR (configs[3]: 64 = 16 x 4), so no row needs a bounds check
+template <bool CPLX, int NR, bool FULL>
 __global__ void __launch_bounds__(kBT) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
@@ -230,8 +231,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
           const int i = j * kBW + hl;
-          xp[j] = i < mi ? gp[i] : Elem<CPLX>::zero();
-          xq[j] = i < mi ? gq[i] : Elem<CPLX>::zero();
+          xp[j] = (FULL || i < mi) ? gp[i] : Elem<CPLX>::zero();
+          xq[j] = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
         }
         int Ep, Eq;
         col_exponents<NR>(xp, xq, Ep, Eq);
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
           const int i = j * kBW + hl;
-          if (i < mi) {
+          if (FULL || i < mi) {
             E a = gp[i], bq = gq[i];
             rot_elem(a, bq, c, Cc, S);
             gp[i] = a;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
 #pragma unroll
     for (int jj = 0; jj < NR; ++jj) {
       const int i = jj * kBW + hl;
-      x[jj] = i < mi ? g[i] : Elem<CPLX>::zero();
+      x[jj] = (FULL || i < mi) ? g[i] : Elem<CPLX>::zero();
       mj = absmax_bits(x[jj], mj);
     }
     mj = hmax_u64(mj);
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       const Pow2 f(-Ej);
 #pragma unroll
       for (int jj = 0; jj < NR; ++jj)
-        if (jj * kBW + hl < mi) sj = ssq_acc(f(x[jj]), sj);
+        if (FULL || jj * kBW + hl < mi) sj = ssq_acc(f(x[jj]), sj);
     }
     sj = hsum(sj);
     double e = -INFINITY, f = 1.0;
@@ -461,13 +462,19 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                                            transforms, Fm, Kr, tol);
   };
   if (cplx) {
-    if (m <= 32) go(batched_svd_kernel<true, 2>);
-    else if (m <= 64) go(batched_svd_kernel<true, 4>);
-    else go(batched_svd_kernel<true, 8>);
+    if (m == 32) go(batched_svd_kernel<true, 2, true>);
+    else if (m == 64) go(batched_svd_kernel<true, 4, true>);
+    else if (m == 128) go(batched_svd_kernel<true, 8, true>);
+    else if (m < 32) go(batched_svd_kernel<true, 2, false>);
+    else if (m < 64) go(batched_svd_kernel<true, 4, false>);
+    else go(batched_svd_kernel<true, 8, false>);
   } else {
-    if (m <= 32) go(batched_svd_kernel<false, 2>);
-    else if (m <= 64) go(batched_svd_kernel<false, 4>);
-    else go(batched_svd_kernel<false, 8>);
+    if (m == 32) go(batched_svd_kernel<false, 2, true>);
+    else if (m == 64) go(batched_svd_kernel<false, 4, true>);
+    else if (m == 128) go(batched_svd_kernel<false, 8, true>);
+    else if (m < 32) go(batched_svd_kernel<false, 2, false>);
+    else if (m < 64) go(batched_svd_kernel<false, 4, false>);
+    else go(batched_svd_kernel<false, 8, false>);
   }
   note_launch();
   e = cudaGetLastError();
