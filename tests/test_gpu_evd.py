@@ -154,3 +154,20 @@ def test_null_zeta_and_perm_and_errors(J):
                                None, None, 0, None) == -1
     assert L.jsvd_evd2_batched(0, 0, None, None, None, None, None, None, None, None, None,
                                None, None, 0, None) == 0
+
+
+def test_real_full_exponent_range_bitwise(J):
+    # the real EVD over configs[1]'s full exponent range (exponents +-1000,
+    # subnormal and near-overflow entries), plus diagonals equal to within a few
+    # ulps (|a11 - a22| tiny or subnormal: tan 2phi clamps or the quotient is
+    # huge) and off-diagonals from 0 to far below them
+    a11, a22, re, _ = synth.evd_cfg2(1 << 20, seed=11)
+    rng = np.random.default_rng(5)
+    n = 1 << 16
+    d = np.ldexp(1 + rng.random(n), rng.integers(-1070, 1020, n))
+    d2 = d * (1 + rng.integers(-4, 5, n) * 2.0 ** -52)
+    off = d * 2.0 ** rng.integers(-1100, 40, n) * np.where(rng.random(n) < 0.5, -1, 1)
+    off[::11] = 0.0
+    arrs = (np.concatenate([a11, d]), np.concatenate([a22, d2]), np.concatenate([re, off]))
+    for flags in (0, 3):
+        _compare(_run(J, arrs, flags), _ref(arrs, flags), False)
