@@ -166,8 +166,11 @@ def test_real_full_exponent_range_bitwise(J):
     n = 1 << 16
     d = np.ldexp(1 + rng.random(n), rng.integers(-1070, 1020, n))
     d2 = d * (1 + rng.integers(-4, 5, n) * 2.0 ** -52)
-    off = d * 2.0 ** rng.integers(-1100, 40, n) * np.where(rng.random(n) < 0.5, -1, 1)
+    ed = np.floor(np.log2(d)).astype(np.int64)
+    k = np.minimum(rng.integers(-1100, 40, n), 1020 - ed)  # finite inputs (the precondition)
+    off = np.ldexp(d, k) * np.where(rng.random(n) < 0.5, -1, 1)
     off[::11] = 0.0
+    assert np.isfinite(off).all() and np.isfinite(d2).all()
     arrs = (np.concatenate([a11, d]), np.concatenate([a22, d2]), np.concatenate([re, off]))
     for flags in (0, 3):
         _compare(_run(J, arrs, flags), _ref(arrs, flags), False)
