@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   __shared__ RedSlot<NW, double> rs_dot;
   __shared__ uint32_t rs_m[NW];
   __shared__ double rot[3];
+  __shared__ TxSlot<CL, int> tx_e;
+  __shared__ TxSlot<CL, double> tx_ssq, tx_dot;
   extern __shared__ __align__(16) unsigned char step_smem[];
   E* sx = reinterpret_cast<E*>(step_smem);  // [NS][2][T]
   const auto sP = [&](int j) -> E& { return sx[(2 * j) * T + threadIdx.x]; };
@@ -63,6 +65,14 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
 
   const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
   const int64_t pair = blockIdx.x / CL;
+  if constexpr (CL > 1) {  // the DSMEM rounds' mbarriers (published before any push)
+    if (threadIdx.x == 0) {
+      txslot_init(tx_e);
+      txslot_init(tx_ssq);
+      txslot_init(tx_dot);
+    }
+    txred_publish();
+  }
   int p, q;
   if (P.pairs) {
     p = P.pairs[2 * pair];
@@ -156,7 +166,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     for (int j = 0; j < NS; ++j) mb = absmax_bits(sQ(j), mb);
     Eq = ilogb_or_min(mb);
   }
-  tree_max2i<T, CL>(Ep, Eq, rs_e);
+  if constexpr (CL > 1) tree_max2i_tx<T, CL>(Ep, Eq, rs_e, tx_e);
+  else tree_max2i<T, 1>(Ep, Eq, rs_e);
   // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform; the
   // two-multiply case 2^-E < 2^-1074 is a uniform branch).  Zero padding adds
   // exact zeros to a non-negative sum.
@@ -195,7 +206,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       for (int j = 0; j < NS; ++j) sq = ssq_acc(scale1(sQ(j), a), sq);
     }
   }
-  tree_sum2<T, CL>(sp, sq, rs_ssq);
+  if constexpr (CL > 1) tree_sum2_tx<T, CL>(sp, sq, rs_ssq, tx_ssq);
+  else tree_sum2<T, 1>(sp, sq, rs_ssq);
   double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
   if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
   if (Eq != kIntMin) ef_from_ssq(Eq, sq, eq, fq);
@@ -227,15 +239,16 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
 #pragma unroll 2
       for (int j = 0; j < NS; ++j) dot_acc(scale1(sQ(j), aq), scale1(sP(j), ap), ar, ai);
     }
-    tree_sum2<T, CL>(ar, ai, rs_dot);
+    if constexpr (CL > 1) tree_sum2_tx<T, CL>(ar, ai, rs_dot, tx_dot);
+    else tree_sum2<T, 1>(ar, ai, rs_dot);
     const Rcp d = rcp_plain(fq * fp);  // fl(f_q f_p) in [1, 4)
     zr = dot_div(ar, d, kFull);
     zi = CPLX ? dot_div(ai, d, kFull) : 0.0;
   }
-  // the last read of a peer CTA's shared memory is done: arrive now, wait at
-  // exit (the wait keeps this CTA's slots alive for its peers)
+  // the last cross-CTA round is done: arrive now, wait at exit (no CTA leaves
+  // while a peer's push into its shared memory could still be in flight)
   if constexpr (CL > 1) {
-    if (!zero_col) __cluster_barrier_arrive();
+    if (!zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   }
   // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
   const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
@@ -362,8 +375,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     P.s_slots[(P.slot + 1) % 3] = P.s_slots[P.slot] + sn;
   }
   if constexpr (CL > 1) {
-    if (zero_col) __cluster_barrier_arrive();  // (no dot: arrive here)
-    __cluster_barrier_wait();  // keep this CTA's shared memory alive for its peers
+    if (zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
   }
 }
 

@@ -163,6 +163,110 @@ __device__ __forceinline__ void tree_max2i(int& a, int& b, RedSlot<T / 32, int>&
   }
 }
 
+// ---- cross-CTA rounds through distributed shared memory without cluster
+// barriers: thread 0 of every CTA pushes the CTA's partial pair into slot
+// [own rank] of every CTA of the cluster with st.async, whose completion
+// (complete_tx) lands on the receiver's mbarrier; each CTA waits on its own
+// mbarrier for all CL partials and folds them in rank order (the CTA bits of R,
+// high to low).  One mbarrier per round (each used once per launch: phase 0).
+// The barriers are initialised and published once per launch (txred_init).
+template <int CL, typename V>
+struct TxSlot {
+  unsigned long long bar;
+  V part[CL][2];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+template <int CL, typename V>
+__device__ __forceinline__ void txslot_init(TxSlot<CL, V>& t) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&t.bar)), "r"(1) : "memory");
+}
+// after every txslot_init of the launch: make the barriers visible to the peers
+__device__ __forceinline__ void txred_publish() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void st_async_pair(uint32_t dst, double a, double b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n"
+               ::"r"(dst), "d"(a), "d"(b), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_pair(uint32_t dst, int a, int b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s32 [%0], {%1, %2}, [%3];\n"
+               ::"r"(dst), "r"(a), "r"(b), "r"(bar) : "memory");
+}
+// the CTA's partial (a, b), known to thread 0 -> every CTA gets all CL partials
+template <int CL, typename V, typename Op>
+__device__ __forceinline__ void tx_exchange(V& a, V& b, TxSlot<CL, V>& t, Op op) {
+  const uint32_t bar = smem_u32(&t.bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 ::"r"(bar), "r"(static_cast<int>(CL * 2 * sizeof(V))) : "memory");
+    const uint32_t me = cg::this_cluster().block_rank();
+    const uint32_t slot = smem_u32(&t.part[me][0]);
+#pragma unroll
+    for (int r = 0; r < CL; ++r) st_async_pair(mapa_u32(slot, r), a, b, mapa_u32(bar, r));
+  }
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(bar), "r"(0) : "memory");
+  } while (!done);
+  V ra[CL], rb[CL];
+#pragma unroll
+  for (int r = 0; r < CL; ++r) {
+    ra[r] = t.part[r][0];
+    rb[r] = t.part[r][1];
+  }
+  a = fold<CL>(ra, op);
+  b = fold<CL>(rb, op);
+}
+
+// tree_sum2 / tree_max2i with the cross-CTA level through tx_exchange
+template <int T, int CL>
+__device__ __forceinline__ void tree_sum2_tx(double& a, double& b, RedSlot<T / 32, double>& s,
+                                             TxSlot<CL, double>& t) {
+  constexpr int NW = T / 32;
+#pragma unroll
+  for (int o = 16; o >= 1; o /= 2) {
+    a = a + __shfl_xor_sync(0xffffffffu, a, o);
+    b = b + __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s.warp[0][w] = a;
+    s.warp[1][w] = b;
+  }
+  __syncthreads();
+  a = fold<NW>(s.warp[0], AddOp());
+  b = fold<NW>(s.warp[1], AddOp());
+  tx_exchange<CL>(a, b, t, AddOp());
+}
+template <int T, int CL>
+__device__ __forceinline__ void tree_max2i_tx(int& a, int& b, RedSlot<T / 32, int>& s,
+                                              TxSlot<CL, int>& t) {
+  constexpr int NW = T / 32;
+  a = __reduce_max_sync(0xffffffffu, a);
+  b = __reduce_max_sync(0xffffffffu, b);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s.warp[0][w] = a;
+    s.warp[1][w] = b;
+  }
+  __syncthreads();
+  a = fold<NW>(s.warp[0], MaxIOp());
+  b = fold<NW>(s.warp[1], MaxIOp());
+  tx_exchange<CL>(a, b, t, MaxIOp());
+}
+
 // CTA-wide max of a u64 (result valid in thread 0 only).
 template <int T>
 __device__ __forceinline__ uint64_t cta_max_u64(uint64_t v, uint64_t* warp_slots) {
