@@ -171,9 +171,9 @@ __device__ __forceinline__ void tree_max2i(int& a, int& b, RedSlot<T / 32, int>&
 // high to low).  One mbarrier per round (each used once per launch: phase 0).
 // The barriers are initialised and published once per launch (txred_init).
 template <int CL, typename V>
-struct TxSlot {
+struct alignas(16) TxSlot {
+  alignas(16) V part[CL][2];  // st.async.v2 targets: 16-byte (f64) / 8-byte (s32) aligned
   unsigned long long bar;
-  V part[CL][2];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
