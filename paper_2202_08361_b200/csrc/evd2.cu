@@ -7,8 +7,6 @@
 // one 16-byte STG.128; the permutation words are assembled from two
 // warp ballots.  No shared memory, no synchronisation.  Grid: one 256-thread
 // CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110 waves at 8 CTAs/SM).
-#include <cstdlib>
-
 #include "jsvd_dev.cuh"
 #include "jsvd_host.h"
 
@@ -93,10 +91,10 @@ __device__ __forceinline__ void evd2_chunk(
   }
 }
 
-// one chunk per CTA (r/512 CTAs); MINB: resident CTAs per SM the register
-// allocation targets
-template <bool CPLX, bool TAN, bool NOBACK, int MINB>
-__global__ void __launch_bounds__(256, MINB) evd2_vec2_kernel(
+// one chunk per CTA (r/512 CTAs) at <= 64 registers: 4 CTAs per SM (a 5-CTA
+// bound spills and measured no better for configs[0], worse for configs[1])
+template <bool CPLX, bool TAN, bool NOBACK>
+__global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
@@ -140,16 +138,8 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     // one 512-matrix chunk per CTA: the measured-best shape for both configs
     // (a persistent grid-stride variant was slower for configs[0] and [1])
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
-    static const int minb = [] {
-      const char* e = getenv("JSVD_EVD_MINB");
-      return e ? atoi(e) : 4;
-    }();
-    if (minb == 5)
-      evd2_vec2_kernel<CPLX, TAN, NOBACK, 5><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
-          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
-    else
-      evd2_vec2_kernel<CPLX, TAN, NOBACK, 4><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
-          r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+    evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
+        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
