@@ -1,7 +1,8 @@
 """Aggregate an ncu SASS source page (CSV) by CUDA source line.
 
 usage: python scripts/ncu_lines.py REPORT.ncu-rep CUBIN_NAME KERNEL_SUBSTR [N]
-  CUBIN_NAME: the cubin inside libjsvd.so (e.g. batched.sm_100a.cubin)
+  CUBIN_NAME: the cubin inside libjsvd.so (e.g. batched.sm_100a.cubin); set
+  JSVD_PROFILED_LIB to the exact .so that was profiled if the tree was rebuilt
 Prints the top-N source lines by warp-stall samples with executed-instruction
 counts (warp level) -- the map from profile to code used for the notes under
 profiles/.  Needs ncu, cuobjdump and nvdisasm (no GPU)."""
@@ -16,7 +17,8 @@ import tempfile
 
 rep, cub, ksub = sys.argv[1], sys.argv[2], sys.argv[3]
 N = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-LIB = os.path.join(os.path.dirname(__file__), "..", "paper_2202_08361_b200", "libjsvd.so")
+LIB = os.environ.get("JSVD_PROFILED_LIB") or os.path.join(os.path.dirname(__file__), "..",
+                                                          "paper_2202_08361_b200", "libjsvd.so")
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
