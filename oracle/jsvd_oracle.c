@@ -398,6 +398,122 @@ int orc_step(int cplx, int64_t m, int64_t n, int64_t nv, double *G, int64_t ldg,
   return ORC_OK;
 }
 
+/* ================================================================ single precision
+ * Alg 2.2 / SM2.1 converted to single precision as the paper prescribes
+ * (P:709-717): omega = FLT_MAX, fl(sqrt(omega)) = 1.844674297E+19,
+ * mu_check = FLT_TRUE_MIN, eta = FLT_MAX_EXP - 4 = 124; every operation in
+ * IEEE binary32 (fmaf, sqrtf, logbf, scalbnf, fminf, fmaxf, copysignf and
+ * float division), otherwise statement for statement the double oracle above.
+ * (NEXT-1 of SURVEY 8(f); the same readings R#1-R#12 apply.)              */
+static uint32_t bits_of_f(float x) { uint32_t u; memcpy(&u, &x, 4); return u; }
+static float of_bits_f(uint32_t u) { float x; memcpy(&x, &u, 4); return x; }
+static float xor_sign_f(float x, float y) { return of_bits_f(bits_of_f(x) ^ (bits_of_f(y) & 0x80000000u)); }
+
+/* fl(sqrt(FLT_MAX)) = 0x1.fffffep+63 = 18446742974197923840 = 1.844674297E+19 */
+static const float SQRT_OMEGA_F = 0x1.fffffep+63f;
+
+float orc_hypot_f32(float x, float y)
+{
+  x = fabsf(x);
+  y = fabsf(y);
+  float m = fminf(x, y), M = fmaxf(x, y);
+  float q = fmaxf(m / M, 0.0f);
+  return sqrtf(fmaf(q, q, 1.0f)) * M;
+}
+
+float orc_zeta_f32(float a11, float a22, float re, float im)
+{
+  const float eta = 124.0f; /* FLT_MAX_EXP - 4 */
+  float z11 = eta - logbf(a11), z22 = eta - logbf(a22);
+  float zr = eta - logbf(re), zi = eta - logbf(im);
+  return fminf(FLT_MAX, fminf(fminf(z11, z22), fminf(zr, zi)));
+}
+
+static int zeta_int_f(float zd) { return zd >= 4096.0f ? 4096 : (int)zd; }
+
+void orc_evd2_one_f32(int is_complex, float a11, float a22, float re, float im, unsigned flags,
+                      float *l1o, float *l2o, float *co, float *sro, float *sio, int32_t *zo,
+                      int *po)
+{
+  if (!is_complex) im = 0.0f;
+  float zd = is_complex ? orc_zeta_f32(a11, a22, re, im) : orc_zeta_f32(a11, a22, re, 0.0f);
+  int iz = zeta_int_f(zd);
+  re = scalbnf(re, iz);
+  if (is_complex) im = scalbnf(im, iz);
+  a11 = scalbnf(a11, iz);
+  a22 = scalbnf(a22, iz);
+  float ab, ca = 0.0f, sa = 0.0f;
+  if (is_complex) {
+    float ar = fabsf(re), ai = fabsf(im);
+    ab = orc_hypot_f32(ar, ai);
+    ca = copysignf(fminf(ar / ab, 1.0f), re);
+    sa = im / fmaxf(ab, FLT_TRUE_MIN);
+  } else {
+    ab = fabsf(re);
+  }
+  float o = scalbnf(ab, 1);
+  float a = a11 - a22;
+  float t2 = copysignf(fminf(fmaxf(o / fabsf(a), 0.0f), SQRT_OMEGA_F), a);
+  float sec2_2 = fmaf(t2, t2, 1.0f);
+  float t = t2 / (1.0f + sqrtf(sec2_2));
+  float s2 = fmaf(t, t, 1.0f);
+  float se = sqrtf(s2);
+  float c = 1.0f / se;
+  float C, S;
+  if (is_complex) {
+    C = ca * t;
+    S = sa * t;
+  } else {
+    C = xor_sign_f(t, re);
+    S = 0.0f;
+  }
+  float l1 = fmaf(t, fmaf(a22, t, o), a11) / s2;
+  float l2 = fmaf(t, fmaf(a11, t, -o), a22) / s2;
+  int p = (l1 < l2);
+  if (!(flags & ORC_EVD_NOBACKSCALE)) {
+    l1 = scalbnf(l1, -iz);
+    l2 = scalbnf(l2, -iz);
+  }
+  float sr, si;
+  if (flags & ORC_EVD_TAN) {
+    sr = C;
+    si = S;
+  } else {
+    sr = C / se;
+    si = S / se;
+  }
+  *l1o = l1;
+  *l2o = l2;
+  *co = c;
+  *sro = sr;
+  if (sio) *sio = si;
+  *zo = (zd == FLT_MAX) ? ORC_ZETA_ZERO : (int32_t)iz;
+  *po = p;
+}
+
+int orc_evd2_batched_f32(int is_complex, int64_t r, const float *a11, const float *a22,
+                         const float *re, const float *im, float *l1, float *l2, float *c,
+                         float *sr, float *si, int32_t *zeta, uint32_t *perm, unsigned flags)
+{
+  if (r < 0 || (is_complex && (!im || !si)) || (!is_complex && (im || si))) return ORC_EINVAL;
+  int64_t nw = (r + 31) / 32;
+#pragma omp parallel for schedule(static)
+  for (int64_t w = 0; w < nw; ++w) {
+    uint32_t word = 0;
+    for (int64_t l = w * 32; l < r && l < (w + 1) * 32; ++l) {
+      int32_t z;
+      int p;
+      float dummy;
+      orc_evd2_one_f32(is_complex, a11[l], a22[l], re[l], is_complex ? im[l] : 0.0f, flags,
+                       &l1[l], &l2[l], &c[l], &sr[l], is_complex ? &si[l] : &dummy, &z, &p);
+      if (zeta) zeta[l] = z;
+      word |= (uint32_t)p << (l % 32);
+    }
+    if (perm) perm[w] = word;
+  }
+  return ORC_OK;
+}
+
 /* ================================================================ strategy
  * R#20.  Flat round-robin (circle method) on P players, round r in [0,P-1):
  * position 0 = player 0, position k>=1 = player ((k-1+r) mod (P-1)) + 1;

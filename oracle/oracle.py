@@ -12,6 +12,7 @@ from .build import LIB, build
 
 __all__ = [
     "RSpec", "lib", "hypot", "zeta", "evd2_one", "evd2_batched", "colnorm", "dot", "cvg",
+    "hypot_f32", "zeta_f32", "evd2_one_f32", "evd2_batched_f32",
     "upsilon", "gram", "rot", "step", "strategy_pairs", "strategy_is_checkpoint", "Fm",
     "gesvj", "gesvj_batched", "num_threads", "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO",
     "OK", "ENOCONV", "EINVAL", "ENONFINITE", "ERANK",
@@ -55,6 +56,16 @@ def lib():
         L.orc_hypot.argtypes = [_D, _D]
         L.orc_zeta.restype = _D
         L.orc_zeta.argtypes = [_D, _D, _D, _D]
+        _F, _PF = ct.c_float, ct.POINTER(ct.c_float)
+        L.orc_hypot_f32.restype = _F
+        L.orc_hypot_f32.argtypes = [_F, _F]
+        L.orc_zeta_f32.restype = _F
+        L.orc_zeta_f32.argtypes = [_F, _F, _F, _F]
+        L.orc_evd2_one_f32.restype = None
+        L.orc_evd2_one_f32.argtypes = [ct.c_int, _F, _F, _F, _F, ct.c_uint, _PF, _PF, _PF, _PF,
+                                       _PF, ct.POINTER(ct.c_int32), ct.POINTER(ct.c_int)]
+        L.orc_evd2_batched_f32.restype = ct.c_int
+        L.orc_evd2_batched_f32.argtypes = [ct.c_int, _I64] + [ct.c_void_p] * 11 + [ct.c_uint]
         L.orc_evd2_one.restype = None
         L.orc_evd2_one.argtypes = [ct.c_int, _D, _D, _D, _D, ct.c_uint, _PD, _PD, _PD, _PD, _PD,
                                    ct.POINTER(ct.c_int32), ct.POINTER(ct.c_int)]
@@ -125,6 +136,46 @@ def evd2_one(is_complex, a11, a22, re, im=0.0, flags=0):
                        flags, *[ct.byref(o) for o in out], ct.byref(z), ct.byref(p))
     l1, l2, c, sr, si = (o.value for o in out)
     return dict(lam1=l1, lam2=l2, cos=c, sin_re=sr, sin_im=si, zeta=z.value, perm=p.value)
+
+
+def hypot_f32(x, y):
+    return float(np.float32(lib().orc_hypot_f32(np.float32(x), np.float32(y))))
+
+
+def zeta_f32(a11, a22, re, im=0.0):
+    return lib().orc_zeta_f32(*[np.float32(v) for v in (a11, a22, re, im)])
+
+
+def evd2_one_f32(is_complex, a11, a22, re, im=0.0, flags=0):
+    out = [ct.c_float() for _ in range(5)]
+    z, p = ct.c_int32(), ct.c_int()
+    lib().orc_evd2_one_f32(int(bool(is_complex)), *[float(np.float32(v)) for v in (a11, a22, re, im)],
+                           flags, *[ct.byref(o) for o in out], ct.byref(z), ct.byref(p))
+    l1, l2, c, sr, si = (np.float32(o.value) for o in out)
+    return dict(lam1=l1, lam2=l2, cos=c, sin_re=sr, sin_im=si, zeta=z.value, perm=p.value)
+
+
+def _f32(x):
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def evd2_batched_f32(a11, a22, a21_re, a21_im=None, flags=0):
+    """Single-precision batched EVD.  Complex iff a21_im is given."""
+    cplx = a21_im is not None
+    a11, a22, re = _f32(a11), _f32(a22), _f32(a21_re)
+    im = _f32(a21_im) if cplx else None
+    r = a11.shape[0]
+    out = {k: np.empty(r, np.float32) for k in ("lam1", "lam2", "cos", "sin_re")}
+    out["sin_im"] = np.empty(r, np.float32) if cplx else None
+    out["zeta"] = np.empty(r, np.int32)
+    out["perm"] = np.empty((r + 31) // 32, np.uint32)
+    p = lambda a: None if a is None else a.ctypes.data_as(ct.c_void_p)  # noqa: E731
+    st = lib().orc_evd2_batched_f32(int(cplx), r, p(a11), p(a22), p(re), p(im), p(out["lam1"]),
+                                    p(out["lam2"]), p(out["cos"]), p(out["sin_re"]),
+                                    p(out["sin_im"]), p(out["zeta"]), p(out["perm"]), flags)
+    if st != OK:
+        raise ValueError(f"orc_evd2_batched_f32 status {st}")
+    return out
 
 
 def evd2_batched(a11, a22, a21_re, a21_im=None, flags=0):
