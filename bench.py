@@ -120,16 +120,23 @@ class EvdWorkload:
         import torch
         import synth
         self.name = name
-        self.cplx = name == "evd_c64"
+        self.cplx = name in ("evd_c64", "evd_c32")
+        self.f32 = name == "evd_c32"
         self.r = (1 << 26) if self.cplx else (1 << 20)
         self.unit = "EVD/s"
-        if self.cplx:
+        if self.f32:
+            self.desc = ("single-precision analogue of BASELINE configs[1] (NEXT-1, P:709-717): "
+                         "batched complex Hermitian 2x2 EVD, fp32, r=2^26 per GPU, seed 7")
+            self.host = synth.evd_cfg2_f32(self.r, off=rank * self.r)
+        elif self.cplx:
             self.desc = "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 per GPU, seed 7"
             self.host = synth.evd_cfg2(self.r, off=rank * self.r)
         else:
             self.desc = "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 per GPU, seed 42"
             self.host = synth.evd_cfg1(self.r, off=rank * self.r)
-        self.unit_bytes = (32 + 40 + 4 + 1 / 8) if self.cplx else (24 + 32 + 4 + 1 / 8)
+        w = 4 if self.f32 else 8
+        self.unit_bytes = (9 * w + 4 + 1 / 8) if self.cplx else (7 * w + 4 + 1 / 8)
+        fdt = torch.float32 if self.f32 else torch.float64
         # configs[0] is 63 MB (< 126 MB L2): the steps cycle through 4 separate
         # input/output sets (252 MB > L2), so every launch streams from HBM
         self.nsets = 1 if self.cplx else 4
@@ -137,7 +144,7 @@ class EvdWorkload:
         self.sets = []
         for _ in range(self.nsets):
             dev = [torch.from_numpy(a).cuda() for a in self.host]
-            out = {k: torch.empty(self.r, dtype=torch.float64, device="cuda") for k in keys}
+            out = {k: torch.empty(self.r, dtype=fdt, device="cuda") for k in keys}
             if not self.cplx:
                 out["sin_im"] = None
             out["zeta"] = torch.empty(self.r, dtype=torch.int32, device="cuda")
@@ -195,8 +202,9 @@ class EvdWorkload:
         import oracle as O
         n = min(self.r, 1 << 20)
         sl = [a[:n] for a in self.host]
-        O.evd2_batched(*[a[:1024] for a in sl])
-        return lambda: O.evd2_batched(*sl), n, f"the first {n} matrices of the batch per call"
+        fn = O.evd2_batched_f32 if self.f32 else O.evd2_batched
+        fn(*[a[:1024] for a in sl])
+        return lambda: fn(*sl), n, f"the first {n} matrices of the batch per call"
 
 
 class StepWorkload:
@@ -574,7 +582,7 @@ class DistC64Workload:
             f"{npairs} of the {self.n // 2} pairs of a step per call (units = fraction of a step)"
 
 
-WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "step_r64": StepWorkload,
+WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "evd_c32": EvdWorkload, "step_r64": StepWorkload,
              "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload,
              "step_c64": StepC64Workload, "dist_c64": DistC64Workload}
 
@@ -742,7 +750,7 @@ def run_jsvd(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f64",
+            "dtype": "f32" if getattr(wl, "f32", False) else "f64",
             "data": "synthetic (counter-based SplitMix64, DESIGN.md recipe)",
             "config": {"workload": wl.desc, "units_per_gpu_step": wl.units_per_step,
                        "timing": ("one CUDA-graph replay of the K steps (CUDA events)" if graph is not None
@@ -782,7 +790,8 @@ def run_reference(args):
         "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": wl.unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32" if args.workload == "evd_c32" else "f64",
+        "data": "synthetic",
         "config": {"workload": wl.desc, "sample_per_step": wl.what},
         "cpu_baseline": {"value": v, "unit": wl.unit, "cores": O.num_threads(),
                          "kind": "oracle", "sample": wl.what},
@@ -797,10 +806,14 @@ class ReferenceWorkload:
     def __init__(self, name):
         import oracle as O
         import synth
-        if name in ("evd_c64", "evd_r64"):  # noqa: SIM114
+        if name in ("evd_c64", "evd_r64", "evd_c32"):  # noqa: SIM114
             n = 1 << 18
-            a = synth.evd_cfg2(n) if name == "evd_c64" else synth.evd_cfg1(n)
-            self.fn = lambda: O.evd2_batched(*a)
+            if name == "evd_c32":
+                a = synth.evd_cfg2_f32(n)
+                self.fn = lambda: O.evd2_batched_f32(*a)
+            else:
+                a = synth.evd_cfg2(n) if name == "evd_c64" else synth.evd_cfg1(n)
+                self.fn = lambda: O.evd2_batched(*a)
             self.units, self.unit = n, "EVD/s"
             self.desc = EvdWorkload.__doc__.strip().split("\n")[0] + f" ({name})"
             self.what = f"{n} matrices of the batch per step"
@@ -818,7 +831,7 @@ class ReferenceWorkload:
             self.what = "one full step (512 pairs) per step"
         else:
             A = synth.svd_cfg4(16)
-            R = O.RSpec.make(32, 1, [16, 8, 4, 2, 1])
+            R = O.RSpec.make(16, 1, [8, 4, 2, 1])  # the batched kernel's R
             self.fn = lambda: O.gesvj_batched(A, R)
             self.units, self.unit = 16, "SVD/s"
             self.desc = "BASELINE configs[3]: complex 64x32 SVDs"
@@ -838,7 +851,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
-        args.steps = {"evd_c64": 200, "evd_r64": 200, "step_r64": 300, "gesvj_r64": 2,
+        args.steps = {"evd_c64": 200, "evd_r64": 200, "evd_c32": 200, "step_r64": 300, "gesvj_r64": 2,
                       "batched_c64": 3, "step_c64": 50, "dist_c64": 100}[args.workload]
     if args.impl == "reference":
         run_reference(args)

@@ -23,7 +23,7 @@ __all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "
            "gesvj_workspace", "gesvj_batched", "launch_count", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
-R64, C64 = 0, 1
+R64, C64, R32, C32 = 0, 1, 2, 3
 EVD_TAN, EVD_NOBACKSCALE = 0x1, 0x2
 ZETA_ZERO = 2 ** 31 - 1
 OK, ENOCONV = 0, 1
@@ -49,6 +49,8 @@ def lib():
         L = ct.CDLL(LIB)
         L.jsvd_evd2_batched.restype = ct.c_int
         L.jsvd_evd2_batched.argtypes = [ct.c_int, _i64] + [_vp] * 11 + [ct.c_uint32, _vp]
+        L.jsvd_evd2_batched_f32.restype = ct.c_int
+        L.jsvd_evd2_batched_f32.argtypes = L.jsvd_evd2_batched.argtypes
         L.jsvd_sweep_step.restype = ct.c_int
         L.jsvd_sweep_step.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _d,
                                       _vp, _vp, _vp, _vp, _vp]
@@ -122,27 +124,35 @@ def _f64(t, name):
 def evd2_batched(a11, a22, a21_re, a21_im=None, flags=0, out=None, stream=None):
     """Batched EVD of 2x2 Hermitian (a21_im given) / symmetric matrices.
 
-    a11, a22, a21_re, a21_im: float64 CUDA tensors of length r (SoA).
+    a11, a22, a21_re, a21_im: float64 (jsvd_evd2_batched) or float32
+    (jsvd_evd2_batched_f32) CUDA tensors of length r (SoA).
     Returns dict(lam1, lam2, cos, sin_re[, sin_im], zeta, perm); pass ``out`` (a
     dict of preallocated tensors with those keys) to avoid allocation.
     """
     cplx = a21_im is not None
     r = a11.numel()
+    dt = a11.dtype
+    if dt not in (torch.float64, torch.float32):
+        raise ValueError("a11 must be a float64 or float32 CUDA tensor")
     for n_, t in (("a11", a11), ("a22", a22), ("a21_re", a21_re)) + ((("a21_im", a21_im),) if cplx else ()):
-        _f64(t, n_)
+        if t.dtype != dt or not t.is_contiguous():
+            raise ValueError(f"{n_} must be a contiguous {dt} CUDA tensor like a11")
         if t.numel() != r:
             raise ValueError("all input streams must have the same length")
     if out is None:
         dev = a11.device
-        out = {k: torch.empty(r, dtype=torch.float64, device=dev) for k in ("lam1", "lam2", "cos", "sin_re")}
-        out["sin_im"] = torch.empty(r, dtype=torch.float64, device=dev) if cplx else None
+        out = {k: torch.empty(r, dtype=dt, device=dev) for k in ("lam1", "lam2", "cos", "sin_re")}
+        out["sin_im"] = torch.empty(r, dtype=dt, device=dev) if cplx else None
         out["zeta"] = torch.empty(r, dtype=torch.int32, device=dev)
         out["perm"] = torch.empty((r + 31) // 32, dtype=torch.int32, device=dev)
-    st = lib().jsvd_evd2_batched(
-        C64 if cplx else R64, r, _p(a11), _p(a22), _p(a21_re), _p(a21_im), _p(out["lam1"]),
-        _p(out["lam2"]), _p(out["cos"]), _p(out["sin_re"]), _p(out.get("sin_im")),
-        _p(out.get("zeta")), _p(out.get("perm")), flags, _stream(stream))
-    _check(st, "jsvd_evd2_batched")
+    if dt == torch.float64:
+        fn, code, name = lib().jsvd_evd2_batched, C64 if cplx else R64, "jsvd_evd2_batched"
+    else:
+        fn, code, name = lib().jsvd_evd2_batched_f32, C32 if cplx else R32, "jsvd_evd2_batched_f32"
+    st = fn(code, r, _p(a11), _p(a22), _p(a21_re), _p(a21_im), _p(out["lam1"]),
+            _p(out["lam2"]), _p(out["cos"]), _p(out["sin_re"]), _p(out.get("sin_im")),
+            _p(out.get("zeta")), _p(out.get("perm")), flags, _stream(stream))
+    _check(st, name)
     return out
 
 

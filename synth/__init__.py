@@ -39,6 +39,8 @@ def _L():
         L.synth_sm64.argtypes = [u64, u64, u64]
         L.synth_evd_cfg1.argtypes = [u64, i64, i64, vp, vp, vp]
         L.synth_evd_cfg2.argtypes = [u64, i64, i64, vp, vp, vp, vp]
+        L.synth_evd_cfg1_f32.argtypes = [u64, i64, i64, vp, vp, vp]
+        L.synth_evd_cfg2_f32.argtypes = [u64, i64, i64, vp, vp, vp, vp]
         L.synth_gauss.argtypes = [u64, u64, i64, i64, vp]
         L.synth_uniform.argtypes = [u64, u64, i64, i64, vp]
         _lib = L
@@ -64,6 +66,20 @@ def evd_cfg2(r, seed=SEEDS[2], off=0):
     """(a11, a22, re, im) float64 arrays of length r: BASELINE configs[1]."""
     a = [np.empty(r, np.float64) for _ in range(4)]
     _L().synth_evd_cfg2(seed, off, r, *map(_p, a))
+    return tuple(a)
+
+
+def evd_cfg1_f32(r, seed=SEEDS[1], off=0):
+    """(a11, a22, a21) float32: the single-precision analogue of configs[0]."""
+    a = [np.empty(r, np.float32) for _ in range(3)]
+    _L().synth_evd_cfg1_f32(seed, off, r, *map(_p, a))
+    return tuple(a)
+
+
+def evd_cfg2_f32(r, seed=SEEDS[2], off=0):
+    """(a11, a22, re, im) float32: the single-precision analogue of configs[1]."""
+    a = [np.empty(r, np.float32) for _ in range(4)]
+    _L().synth_evd_cfg2_f32(seed, off, r, *map(_p, a))
     return tuple(a)
 
 

@@ -92,6 +92,72 @@ void synth_evd_cfg2(uint64_t seed, int64_t off, int64_t r, double *a11, double *
   }
 }
 
+/* ---- single-precision analogues (the fp32 EVD, NEXT-1): binary32 values
+ * +-m 2^e with m ~ U[1,2) (23 random bits); configs[0]-like: e ~ U{-20..20},
+ * 1% specials {one entry -> +0, a21 -> random nonzero subnormal, one entry ->
+ * +-m 2^124}; configs[1]-like: e ~ U{-120..120} (the float exponent range as
+ * configs[1]'s +-1000 is the double's), 2% both Re and Im a21 subnormal, 1% one
+ * component -> +-m 2^127.                                                    */
+static float of_bits_f(uint32_t u) { float x; memcpy(&x, &u, 4); return x; }
+static float signed_pow2_f(uint64_t u, int lo, int hi)
+{
+  float m = 1.0f + (float)((u >> 11) & 0x7FFFFFull) * 0x1p-23f;
+  int e = lo + (int)((u & 0x7FFull) % (uint64_t)(hi - lo + 1));
+  float v = ldexpf(m, e);
+  return (u >> 63) ? -v : v;
+}
+static float random_subnormal_f(uint64_t u)
+{
+  float v = of_bits_f((uint32_t)(u & 0x7FFFFFull) | 1u);
+  return (u >> 63) ? -v : v;
+}
+
+void synth_evd_cfg1_f32(uint64_t seed, int64_t off, int64_t r, float *a11, float *a22, float *a21)
+{
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < r; ++k) {
+    uint64_t l = (uint64_t)(off + k);
+    float v[3];
+    for (int s = 0; s < 3; ++s) v[s] = signed_pow2_f(synth_sm64(seed, (uint64_t)s, l), -20, 20);
+    uint64_t u = synth_sm64(seed, 8, l);
+    if (u % 100 == 0) {
+      uint64_t w = synth_sm64(seed, 9, l);
+      int kind = (int)((u >> 32) % 3), ent = (int)((u >> 40) % 3);
+      if (kind == 0) v[ent] = 0.0f;
+      else if (kind == 1) v[2] = random_subnormal_f(w);
+      else v[ent] = signed_pow2_f(w & ~0x7FFull, 124, 124);
+    }
+    a11[k] = v[0];
+    a22[k] = v[1];
+    a21[k] = v[2];
+  }
+}
+
+void synth_evd_cfg2_f32(uint64_t seed, int64_t off, int64_t r, float *a11, float *a22, float *re,
+                        float *im)
+{
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < r; ++k) {
+    uint64_t l = (uint64_t)(off + k);
+    float v[4];
+    for (int s = 0; s < 4; ++s)
+      v[s] = signed_pow2_f(synth_sm64(seed, (uint64_t)s, l), -120, 120);
+    uint64_t u = synth_sm64(seed, 8, l);
+    uint64_t x = u % 100;
+    if (x < 2) {
+      v[2] = random_subnormal_f(synth_sm64(seed, 9, l));
+      v[3] = random_subnormal_f(synth_sm64(seed, 10, l));
+    } else if (x == 2) {
+      int ent = (int)((u >> 40) % 4);
+      v[ent] = signed_pow2_f(synth_sm64(seed, 9, l) & ~0x7FFull, 127, 127);
+    }
+    a11[k] = v[0];
+    a22[k] = v[1];
+    re[k] = v[2];
+    im[k] = v[3];
+  }
+}
+
 /* N(0,1) by Box-Muller: out[k] = sqrt(-2 ln u1) cos(2 pi u2), u in (0,1],
  * u1, u2 from indices 2(off+k), 2(off+k)+1 of the stream.                   */
 void synth_gauss(uint64_t seed, uint64_t stream, int64_t off, int64_t count, double *out)
