@@ -153,7 +153,7 @@ class EvdWorkload:
         self.dev, self.out = self.sets[0]
         self.k = 0
         self.units_per_step = self.r
-        self.kernel = "evd2_vec2_kernel"
+        self.kernel = "evd2f_vec4_kernel" if self.f32 else "evd2_vec2_kernel"
         self.l2_note = ("inputs+outputs %.1f GB per step > 126 MB L2 (no flush needed)"
                         % (self.unit_bytes * self.r / 1e9)) if self.cplx else \
             "63 MB per step; steps cycle through 4 input/output sets (252 MB > 126 MB L2)"
