@@ -204,3 +204,32 @@ def test_config4_batched_sampled_bitwise(J):
     # north_star tolerances on the GPU result: sigma vs LAPACK, residual, orthogonality
     s = np.linalg.svd(A[idx], compute_uv=False)
     assert (np.abs(out["sigma"][idx].cpu().numpy() - s) / s).max() <= 1e-12
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("max_sweeps", [2, 40])
+def test_gesvj_batched_mixed_status_and_caps(J, cplx, max_sweeps):
+    # matrices that stop at different sweeps share CTAs (two per CTA for n <= 32):
+    # a zero matrix (ERANK), a non-finite one (ENONFINITE), an already
+    # orthogonal one (1 sweep), capped runs (ENOCONV) next to converging ones
+    rng = np.random.default_rng(90 + cplx + max_sweeps)
+    b, m, n = 7, 40, 24
+    A = rng.standard_normal((b, m, n)) * 2.0 ** rng.integers(-30, 30, (b, 1, n))
+    if cplx:
+        A = A + 1j * rng.standard_normal((b, m, n))
+    A[2] = 0.0
+    A[3, 5, 7] = np.nan
+    Q, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    A[4] = Q * 2.0 ** np.arange(n)[None, :]  # orthogonal columns with distinct norms
+    W, c, offs = J.batched_rspec(cplx, m)
+    ref = O.gesvj_batched(A, O.RSpec.make(W, c, offs), max_sweeps=max_sweeps)
+    g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+    out = J.gesvj_batched(g, max_sweeps=max_sweeps)
+    torch.cuda.synchronize()
+    assert np.array_equal(out["status"].cpu().numpy(), ref["status"])
+    assert np.array_equal(out["sweeps"].cpu().numpy(), ref["sweeps"])
+    ok = [k for k in range(b) if ref["status"][k] >= 0]
+    U = out["U"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+    V = out["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+    assert bits_equal(U[ok], ref["U"][ok]) and bits_equal(V[ok], ref["V"][ok])
+    assert bits_equal(out["sigma"].cpu().numpy()[ok], ref["sigma"][ok])
