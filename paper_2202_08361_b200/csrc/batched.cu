@@ -418,20 +418,21 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   }
 }
 
-// Two matrices per CTA in lockstep (n <= 32, i.e. at most 16 pairs each):
-// phase B then batches the EVDs of BOTH matrices' steps across the 32 lanes of
+// Two matrices per 512-thread CTA in lockstep (n <= 32, i.e. at most 16 pairs
+// each): half-warps 0-15 serve matrix 0 and 16-31 matrix 1 in phases A and C,
+// and phase B batches the EVDs of BOTH matrices' steps across the 32 lanes of
 // warp 0 -- the latency of the one-warp phase is paid once per two matrix-
-// steps -- and phases A and C run two rounds of 16 half-warp pairs.  Per
-// matrix everything (arithmetic, order, checks, stopping) is exactly the
-// one-matrix kernel's: a matrix that has converged stops working while its
-// partner continues.
+// steps.  Per matrix everything (arithmetic, order, checks, stopping) is
+// exactly the one-matrix kernel's: a matrix that has converged stops working
+// while its partner continues.
 template <bool CPLX, int NR, bool FULL>
-__global__ void __launch_bounds__(kBT) batched_svd2_kernel(
+__global__ void __launch_bounds__(2 * kBT) batched_svd2_kernel(
     int64_t batch, int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg,
     int64_t ldv, int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out,
     int32_t* status_out, int64_t* transforms_out, int Fm, int Kr, double tol) {
   using E = typename Elem<CPLX>::T;
   constexpr int MPC = 2;
+  constexpr int T2 = MPC * kBT;  // 512 threads, 32 half-warps
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mi = static_cast<int>(m), ni = static_cast<int>(n);
   const int np = ni / 2;  // <= 16
@@ -444,12 +445,12 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
   __shared__ unsigned long long sM0[MPC];
   __shared__ uint32_t sMt[MPC];
   __shared__ int sT[MPC];
-  __shared__ uint64_t wred[kBNW];
+  __shared__ uint64_t wred[T2 / 32];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4;
   const int64_t b0 = MPC * static_cast<int64_t>(blockIdx.x);
-  for (int k = threadIdx.x; k < (ni - 1) * np; k += kBT) {
+  for (int k = threadIdx.x; k < (ni - 1) * np; k += T2) {
     int p, q;
     strategy_pair(ni, ni, k / np, k % np, p, q);
     sPairs[2 * k] = static_cast<uint8_t>(p);
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
     uint64_t mx = 0;
     if (exists) {
       const E* Ag = reinterpret_cast<const E*>(A) + (b0 + mm) * strideA;
-      for (int k = threadIdx.x; k < mi * ni; k += kBT) {
+      for (int k = threadIdx.x; k < mi * ni; k += T2) {
         const int j = k / mi, i = k - j * mi;
         const E x = Ag[static_cast<int64_t>(j) * lda + i];
         G(mm)[k] = x;
@@ -478,13 +479,13 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
           mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
         }
       }
-      for (int k = threadIdx.x; k < ni * ni; k += kBT) {
+      for (int k = threadIdx.x; k < ni * ni; k += T2) {
         const int j = k / ni, i = k - j * ni;
         if constexpr (CPLX) Vs(mm)[k] = make_double2(i == j ? 1.0 : 0.0, 0.0);
         else Vs(mm)[k] = i == j ? 1.0 : 0.0;
       }
     }
-    const uint64_t M0 = cta_max_u64<kBT>(mx, wred);
+    const uint64_t M0 = cta_max_u64<T2>(mx, wred);
     if (threadIdx.x == 0) sM0[mm] = M0;
     __syncthreads();
     const double M0d = __longlong_as_double(static_cast<long long>(sM0[mm]));
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
     if (live[mm]) {  // line 1: s0 = F(m) - floor(lg M0) - 1; G1 = 2^s0 G
       s_[mm] = Fm - ilogb_bits(sM0[mm]) - 1;
       const int s0 = s_[mm];
-      for (int k = threadIdx.x; k < mi * ni; k += kBT) {
+      for (int k = threadIdx.x; k < mi * ni; k += T2) {
         if constexpr (CPLX) G(mm)[k] = make_double2(scalbn_rn(G(mm)[k].x, s0), scalbn_rn(G(mm)[k].y, s0));
         else G(mm)[k] = scalbn_rn(G(mm)[k], s0);
       }
@@ -542,7 +543,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
         const int sn = (Kr - lm < 0) ? Fm - lm - 1 : 0;
         if (sn != 0) {  // uniform
           __syncthreads();
-          for (int kk = threadIdx.x; kk < mi * ni; kk += kBT) {
+          for (int kk = threadIdx.x; kk < mi * ni; kk += T2) {
             if constexpr (CPLX) G(mm)[kk] = make_double2(scalbn_rn(G(mm)[kk].x, sn), scalbn_rn(G(mm)[kk].y, sn));
             else G(mm)[kk] = scalbn_rn(G(mm)[kk], sn);
           }
@@ -552,49 +553,48 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
           __syncthreads();
         }
       }
-      // ---- phase A: one round per matrix, half-warp per pair
+      // ---- phase A: half-warp hw serves pair hw & 15 of matrix hw >> 4
+      {
+        const int mm = hw >> 4, l = hw & 15;
+        if (done[mm]) {  // (uniform per 16 half-warps) a finished matrix says "no transform"
+          if (hl == 0) slots[hw].transform = 0;
+        } else {
+          const bool act = l < np;
+          const int p = act ? sPairs[2 * (k * np + l)] : 0;
+          const int q = act ? sPairs[2 * (k * np + l) + 1] : 1;
+          const E* gp = G(mm) + p * mi;
+          const E* gq = G(mm) + q * mi;
+          E xp[NR], xq[NR];
 #pragma unroll
-      for (int mm = 0; mm < MPC; ++mm) {
-        if (done[mm]) {  // uniform: a finished matrix's slots say "no transform"
-          if (hl == 0) slots[mm * 16 + hw].transform = 0;
-          continue;
-        }
-        const int l = hw;
-        const bool act = l < np;
-        const int p = act ? sPairs[2 * (k * np + l)] : 0;
-        const int q = act ? sPairs[2 * (k * np + l) + 1] : 1;
-        const E* gp = G(mm) + p * mi;
-        const E* gq = G(mm) + q * mi;
-        E xp[NR], xq[NR];
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          const int i = j * kBW + hl;
-          xp[j] = (FULL || i < mi) ? gp[i] : Elem<CPLX>::zero();
-          xq[j] = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
-        }
-        int Ep, Eq;
-        col_exponents<NR>(xp, xq, Ep, Eq);
-        double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
-        double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
-        sp = hsum(sp);
-        sq = hsum(sq);
-        int ep = kIntMin, eq = kIntMin;
-        double gpv = 1.0, gqv = 1.0;
-        if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
-        if (Eq != kIntMin) eg_from_ssq(Eq, sq, eq, gqv);
-        const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);
-        double ar = 0.0, ai = 0.0;
-        if (!zero_col) dot_lane<NR>(xq, xp, eq, ep, ar, ai);
-        ar = hsum(ar);
-        if (CPLX) ai = hsum(ai);
-        if (act && hl == 0) {
-          PairSlot& sl = slots[mm * 16 + l];
-          sl.ar = zero_col ? 0.0 : ar;
-          sl.ai = zero_col ? 0.0 : ai;
-          sl.gp = gpv;
-          sl.gq = gqv;
-          sl.ep = ep;
-          sl.eq = eq;
+          for (int j = 0; j < NR; ++j) {
+            const int i = j * kBW + hl;
+            xp[j] = (FULL || i < mi) ? gp[i] : Elem<CPLX>::zero();
+            xq[j] = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
+          }
+          int Ep, Eq;
+          col_exponents<NR>(xp, xq, Ep, Eq);
+          double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
+          double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
+          sp = hsum(sp);
+          sq = hsum(sq);
+          int ep = kIntMin, eq = kIntMin;
+          double gpv = 1.0, gqv = 1.0;
+          if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
+          if (Eq != kIntMin) eg_from_ssq(Eq, sq, eq, gqv);
+          const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);
+          double ar = 0.0, ai = 0.0;
+          if (!zero_col) dot_lane<NR>(xq, xp, eq, ep, ar, ai);
+          ar = hsum(ar);
+          if (CPLX) ai = hsum(ai);
+          if (act && hl == 0) {
+            PairSlot& sl = slots[hw];
+            sl.ar = zero_col ? 0.0 : ar;
+            sl.ai = zero_col ? 0.0 : ai;
+            sl.gp = gpv;
+            sl.gq = gqv;
+            sl.ep = ep;
+            sl.eq = eq;
+          }
         }
       }
       __syncthreads();
@@ -629,18 +629,16 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
           sT[0] += __popc(bal & 0xffffu);
           sT[1] += __popc(bal >> 16);
         }
-      } else if (pend_k >= 0) {  // half-warps 2..15: V of the previous step
-        rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw - 2, kBNH - 2);
+      } else if (pend_k >= 0) {  // half-warps 2..31: V of the previous step
+        rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw - 2, 2 * kBNH - 2);
       }
       __syncthreads();
-      // ---- phase C: rotations of G, one round per matrix
-#pragma unroll
-      for (int mm = 0; mm < MPC; ++mm) {
-        if (done[mm]) continue;
+      // ---- phase C: rotations of G (half-warp hw: pair hw & 15 of matrix hw >> 4)
+      {
+        const int mm = hw >> 4, l = hw & 15;
         uint32_t Mw = 0;
-        const int l = hw;
-        if (l < np) {
-          const PairSlot& sl = slots[mm * 16 + l];
+        if (!done[mm] && l < np) {
+          const PairSlot& sl = slots[hw];
           if (sl.transform) {
             const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
             const double c = sl.c, Cc = sl.C, S = sl.S;
@@ -663,7 +661,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
             }
           }
         }
-        Mw = __reduce_max_sync(0xffffffffu, Mw);
+        Mw = __reduce_max_sync(0xffffffffu, Mw);  // a warp serves one matrix
         if (lane == 0 && Mw > sMt[mm]) atomicMax(&sMt[mm], Mw);
       }
       pend_k = k;
@@ -683,7 +681,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
     __syncthreads();
   }
   if (pend_k >= 0) {  // the last step's V rotations
-    rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw, kBNH);
+    rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw, 2 * kBNH);
     __syncthreads();
   }
   // ---- finalize per matrix
@@ -693,7 +691,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
     const int64_t b = b0 + mm;
     double* ce = ceb + mm * ni;
     double* cf = cfb + mm * ni;
-    for (int j0 = 0; j0 < ni; j0 += kBNH) {
+    for (int j0 = 0; j0 < ni; j0 += 2 * kBNH) {
       const int j = j0 + hw;
       const bool act = j < ni;
       const E* g = G(mm) + (act ? j : 0) * mi;
@@ -725,7 +723,7 @@ __global__ void __launch_bounds__(kBT) batched_svd2_kernel(
     __syncthreads();
     E* Ag = reinterpret_cast<E*>(A) + b * strideA;
     E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
-    for (int r0 = warp; r0 < ni; r0 += kBNW) {
+    for (int r0 = warp; r0 < ni; r0 += 2 * kBNW) {
       int jsel = 0;
       for (int j = lane; j < ni; j += 32) {
         const double ej = ce[j], fj = cf[j];
@@ -822,7 +820,7 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
   const bool two = n <= 32 && batch >= 2 && smem2 <= 220 * 1024;
   auto go2 = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
-    kern<<<static_cast<unsigned>((batch + 1) / 2), kBT, smem2, st>>>(
+    kern<<<static_cast<unsigned>((batch + 1) / 2), 2 * kBT, smem2, st>>>(
         batch, m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps, sweeps_done, status,
         transforms, Fm, Kr, tol);
   };
