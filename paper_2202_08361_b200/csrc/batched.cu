@@ -418,360 +418,6 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   }
 }
 
-// Two matrices per 512-thread CTA in lockstep (n <= 32, i.e. at most 16 pairs
-// each): half-warps 0-15 serve matrix 0 and 16-31 matrix 1 in phases A and C,
-// and phase B batches the EVDs of BOTH matrices' steps across the 32 lanes of
-// warp 0 -- the latency of the one-warp phase is paid once per two matrix-
-// steps.  Per matrix everything (arithmetic, order, checks, stopping) is
-// exactly the one-matrix kernel's: a matrix that has converged stops working
-// while its partner continues.
-template <bool CPLX, int NR, bool FULL>
-__global__ void __launch_bounds__(2 * kBT) batched_svd2_kernel(
-    int64_t batch, int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg,
-    int64_t ldv, int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out,
-    int32_t* status_out, int64_t* transforms_out, int Fm, int Kr, double tol) {
-  using E = typename Elem<CPLX>::T;
-  constexpr int MPC = 2;
-  constexpr int T2 = MPC * kBT;  // 512 threads, 32 half-warps
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int mi = static_cast<int>(m), ni = static_cast<int>(n);
-  const int np = ni / 2;  // <= 16
-  E* sGb = reinterpret_cast<E*>(smem_raw);                // [MPC][n][m]
-  E* sVb = sGb + MPC * mi * ni;                           // [MPC][n][n]
-  PairSlot* slots2 = reinterpret_cast<PairSlot*>(sVb + MPC * ni * ni);  // [2 steps][MPC][16]
-  double* ceb = reinterpret_cast<double*>(slots2 + 2 * MPC * 16);        // [MPC][n]
-  double* cfb = ceb + MPC * ni;
-  uint8_t* sPairs = reinterpret_cast<uint8_t*>(cfb + MPC * ni);
-  __shared__ unsigned long long sM0[MPC];
-  __shared__ uint32_t sMt[MPC];
-  __shared__ int sT[MPC];
-  __shared__ uint64_t wred[T2 / 32];
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4;
-  const int64_t b0 = MPC * static_cast<int64_t>(blockIdx.x);
-  for (int k = threadIdx.x; k < (ni - 1) * np; k += T2) {
-    int p, q;
-    strategy_pair(ni, ni, k / np, k % np, p, q);
-    sPairs[2 * k] = static_cast<uint8_t>(p);
-    sPairs[2 * k + 1] = static_cast<uint8_t>(q);
-  }
-  const auto G = [&](int mm) { return sGb + mm * mi * ni; };
-  const auto Vs = [&](int mm) { return sVb + mm * ni * ni; };
-
-  // ---- load A, M0, V = I (per matrix); a missing second matrix is "done"
-  bool done[MPC], live[MPC];
-  int s_[MPC];
-#pragma unroll
-  for (int mm = 0; mm < MPC; ++mm) {
-    const bool exists = b0 + mm < batch;
-    uint64_t mx = 0;
-    if (exists) {
-      const E* Ag = reinterpret_cast<const E*>(A) + (b0 + mm) * strideA;
-      for (int k = threadIdx.x; k < mi * ni; k += T2) {
-        const int j = k / mi, i = k - j * mi;
-        const E x = Ag[static_cast<int64_t>(j) * lda + i];
-        G(mm)[k] = x;
-        if constexpr (CPLX) {
-          mx = max(mx, abs_bits(fmin(fabs(x.x), static_cast<double>(INFINITY))));
-          mx = max(mx, abs_bits(fmin(fabs(x.y), static_cast<double>(INFINITY))));
-        } else {
-          mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
-        }
-      }
-      for (int k = threadIdx.x; k < ni * ni; k += T2) {
-        const int j = k / ni, i = k - j * ni;
-        if constexpr (CPLX) Vs(mm)[k] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-        else Vs(mm)[k] = i == j ? 1.0 : 0.0;
-      }
-    }
-    const uint64_t M0 = cta_max_u64<T2>(mx, wred);
-    if (threadIdx.x == 0) sM0[mm] = M0;
-    __syncthreads();
-    const double M0d = __longlong_as_double(static_cast<long long>(sM0[mm]));
-    live[mm] = exists && !(isinf(M0d) || M0d == 0.0);
-    done[mm] = !live[mm];
-    if (exists && !live[mm] && threadIdx.x == 0) {
-      if (status_out) status_out[b0 + mm] = isinf(M0d) ? JSVD_ENONFINITE : JSVD_ERANK;
-      if (sweeps_out) sweeps_out[b0 + mm] = 0;
-      if (transforms_out) transforms_out[b0 + mm] = 0;
-    }
-    s_[mm] = 0;
-    if (live[mm]) {  // line 1: s0 = F(m) - floor(lg M0) - 1; G1 = 2^s0 G
-      s_[mm] = Fm - ilogb_bits(sM0[mm]) - 1;
-      const int s0 = s_[mm];
-      for (int k = threadIdx.x; k < mi * ni; k += T2) {
-        if constexpr (CPLX) G(mm)[k] = make_double2(scalbn_rn(G(mm)[k].x, s0), scalbn_rn(G(mm)[k].y, s0));
-        else G(mm)[k] = scalbn_rn(G(mm)[k], s0);
-      }
-      if (threadIdx.x == 0) sMt[mm] = hi32(scalbn_rn(M0d, s0));
-    }
-    __syncthreads();
-  }
-
-  const auto rotate_v = [&](const PairSlot* sl_, int kstep, int g_begin, int g_step) {
-    for (int g = g_begin; g < MPC * 16; g += g_step) {
-      const int mm = g >> 4, l = g & 15;
-      if (l >= np) continue;
-      const PairSlot& sl = sl_[g];
-      if (!sl.transform) continue;
-      const int p = sPairs[2 * (kstep * np + l)], q = sPairs[2 * (kstep * np + l) + 1];
-      E* vp = Vs(mm) + p * ni;
-      E* vq = Vs(mm) + q * ni;
-      for (int i = hl; i < ni; i += kBW) {
-        E a = vp[i], bq = vq[i];
-        rot_elem(a, bq, sl.c, sl.C, sl.S);
-        vp[i] = a;
-        vq[i] = bq;
-      }
-    }
-  };
-  int pend_k = -1, pend_buf = 0;
-  int gstep = 0;
-  int sweeps[MPC] = {0, 0};
-  bool conv[MPC] = {false, false};
-  int64_t Ttot[MPC] = {0, 0};
-  for (int C = 0; C < max_sweeps && !(done[0] && done[1]); ++C) {
-    if (threadIdx.x < MPC) sT[threadIdx.x] = 0;
-    for (int k = 0; k < ni - 1; ++k, ++gstep) {
-      PairSlot* slots = slots2 + (gstep & 1) * (MPC * 16);
-      // ---- line 6: rescale check per matrix (every step for flat round-robin)
-#pragma unroll
-      for (int mm = 0; mm < MPC; ++mm) {
-        if (done[mm]) continue;
-        const int lm = static_cast<int>(sMt[mm] >> 20) - 1023;
-        const int sn = (Kr - lm < 0) ? Fm - lm - 1 : 0;
-        if (sn != 0) {  // uniform
-          __syncthreads();
-          for (int kk = threadIdx.x; kk < mi * ni; kk += T2) {
-            if constexpr (CPLX) G(mm)[kk] = make_double2(scalbn_rn(G(mm)[kk].x, sn), scalbn_rn(G(mm)[kk].y, sn));
-            else G(mm)[kk] = scalbn_rn(G(mm)[kk], sn);
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) sMt[mm] = hi32(scalbn_rn(mkd(sMt[mm], 0u), sn));
-          s_[mm] += sn;
-          __syncthreads();
-        }
-      }
-      // ---- phase A: half-warp hw serves pair hw & 15 of matrix hw >> 4
-      {
-        const int mm = hw >> 4, l = hw & 15;
-        if (done[mm]) {  // (uniform per 16 half-warps) a finished matrix says "no transform"
-          if (hl == 0) slots[hw].transform = 0;
-        } else {
-          const bool act = l < np;
-          const int p = act ? sPairs[2 * (k * np + l)] : 0;
-          const int q = act ? sPairs[2 * (k * np + l) + 1] : 1;
-          const E* gp = G(mm) + p * mi;
-          const E* gq = G(mm) + q * mi;
-          E xp[NR], xq[NR];
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const int i = j * kBW + hl;
-            xp[j] = (FULL || i < mi) ? gp[i] : Elem<CPLX>::zero();
-            xq[j] = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
-          }
-          int Ep, Eq;
-          col_exponents<NR>(xp, xq, Ep, Eq);
-          double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
-          double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
-          sp = hsum(sp);
-          sq = hsum(sq);
-          int ep = kIntMin, eq = kIntMin;
-          double gpv = 1.0, gqv = 1.0;
-          if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
-          if (Eq != kIntMin) eg_from_ssq(Eq, sq, eq, gqv);
-          const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);
-          double ar = 0.0, ai = 0.0;
-          if (!zero_col) dot_lane<NR>(xq, xp, eq, ep, ar, ai);
-          ar = hsum(ar);
-          if (CPLX) ai = hsum(ai);
-          if (act && hl == 0) {
-            PairSlot& sl = slots[hw];
-            sl.ar = zero_col ? 0.0 : ar;
-            sl.ai = zero_col ? 0.0 : ai;
-            sl.gp = gpv;
-            sl.gq = gqv;
-            sl.ep = ep;
-            sl.eq = eq;
-          }
-        }
-      }
-      __syncthreads();
-      // ---- phase B: both matrices' Grammians + EVDs, lane g = 16 mm + l
-      if (warp == 0) {
-        const int mm = lane >> 4, l = lane & 15;
-        const bool act = l < np && !done[mm];
-        const PairSlot& s0 = slots[act ? lane : 0];
-        const bool zp = !act || s0.ep == kIntMin, zq = !act || s0.eq == kIntMin;
-        const double fp = zp ? 1.0 : sqrt_plain(s0.gp), fq = zq ? 1.0 : sqrt_plain(s0.gq);
-        const double ep = zp ? -INFINITY : static_cast<double>(s0.ep);
-        const double eq = zq ? -INFINITY : static_cast<double>(s0.eq);
-        const Rcp d = rcp_plain(fq * fp);
-        const double zr = dot_div(act ? s0.ar : 0.0, d, kFull);
-        const double zi = CPLX ? dot_div(act ? s0.ai : 0.0, d, kFull) : 0.0;
-        const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
-        const bool tr = act && !(zp || zq) && tol <= az;  // Alg 3.2
-        if (__any_sync(kFull, tr)) {
-          double b11, b22, br, bi;
-          gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
-                    tr ? fq : 1.0, b11, b22, br, bi, kFull);
-          const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);
-          if (tr) {
-            slots[lane].c = o.c;
-            slots[lane].C = o.sr;
-            slots[lane].S = o.si;
-          }
-        }
-        if (l < np) slots[lane].transform = tr;
-        const uint32_t bal = __ballot_sync(0xffffffffu, tr);
-        if (lane == 0) {
-          sT[0] += __popc(bal & 0xffffu);
-          sT[1] += __popc(bal >> 16);
-        }
-      } else if (pend_k >= 0) {  // half-warps 2..31: V of the previous step
-        rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw - 2, 2 * kBNH - 2);
-      }
-      __syncthreads();
-      // ---- phase C: rotations of G (half-warp hw: pair hw & 15 of matrix hw >> 4)
-      {
-        const int mm = hw >> 4, l = hw & 15;
-        uint32_t Mw = 0;
-        if (!done[mm] && l < np) {
-          const PairSlot& sl = slots[hw];
-          if (sl.transform) {
-            const int p = sPairs[2 * (k * np + l)], q = sPairs[2 * (k * np + l) + 1];
-            const double c = sl.c, Cc = sl.C, S = sl.S;
-            E* gp = G(mm) + p * mi;
-            E* gq = G(mm) + q * mi;
-            const bool track = max(sl.ep, sl.eq) > Kr - 1;  // see the one-matrix kernel
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-              const int i = j * kBW + hl;
-              if (FULL || i < mi) {
-                E a = gp[i], bq = gq[i];
-                rot_elem(a, bq, c, Cc, S);
-                gp[i] = a;
-                gq[i] = bq;
-                if (track) {
-                  Mw = hi_max(a, Mw);
-                  Mw = hi_max(bq, Mw);
-                }
-              }
-            }
-          }
-        }
-        Mw = __reduce_max_sync(0xffffffffu, Mw);  // a warp serves one matrix
-        if (lane == 0 && Mw > sMt[mm]) atomicMax(&sMt[mm], Mw);
-      }
-      pend_k = k;
-      pend_buf = gstep & 1;
-      __syncthreads();
-    }
-#pragma unroll
-    for (int mm = 0; mm < MPC; ++mm) {
-      if (done[mm]) continue;
-      Ttot[mm] += sT[mm];
-      sweeps[mm] = C + 1;
-      if (sT[mm] == 0) {
-        conv[mm] = true;
-        done[mm] = true;
-      }
-    }
-    __syncthreads();
-  }
-  if (pend_k >= 0) {  // the last step's V rotations
-    rotate_v(slots2 + pend_buf * (MPC * 16), pend_k, hw, 2 * kBNH);
-    __syncthreads();
-  }
-  // ---- finalize per matrix
-#pragma unroll
-  for (int mm = 0; mm < MPC; ++mm) {
-    if (!live[mm]) continue;
-    const int64_t b = b0 + mm;
-    double* ce = ceb + mm * ni;
-    double* cf = cfb + mm * ni;
-    for (int j0 = 0; j0 < ni; j0 += 2 * kBNH) {
-      const int j = j0 + hw;
-      const bool act = j < ni;
-      const E* g = G(mm) + (act ? j : 0) * mi;
-      E x[NR];
-      uint64_t mj = 0;
-#pragma unroll
-      for (int jj = 0; jj < NR; ++jj) {
-        const int i = jj * kBW + hl;
-        x[jj] = (FULL || i < mi) ? g[i] : Elem<CPLX>::zero();
-        mj = absmax_bits(x[jj], mj);
-      }
-      mj = hmax_u64(mj);
-      const int Ej = ilogb_or_min(mj);
-      double sj = 0.0;
-      if (Ej != kIntMin) {
-        const Pow2 f(-Ej);
-#pragma unroll
-        for (int jj = 0; jj < NR; ++jj)
-          if (FULL || jj * kBW + hl < mi) sj = ssq_acc(f(x[jj]), sj);
-      }
-      sj = hsum(sj);
-      double e = -INFINITY, f = 1.0;
-      if (Ej != kIntMin) ef_from_ssq(Ej, sj, e, f);
-      if (act && hl == 0) {
-        ce[j] = e;
-        cf[j] = f;
-      }
-    }
-    __syncthreads();
-    E* Ag = reinterpret_cast<E*>(A) + b * strideA;
-    E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
-    for (int r0 = warp; r0 < ni; r0 += 2 * kBNW) {
-      int jsel = 0;
-      for (int j = lane; j < ni; j += 32) {
-        const double ej = ce[j], fj = cf[j];
-        int rank = 0;
-        for (int kk = 0; kk < ni; ++kk) {
-          const double ek = ce[kk], fk = cf[kk];
-          rank += ((ek > ej) || (ek == ej && (fk > fj || (fk == fj && kk < j)))) ? 1 : 0;
-        }
-        if (rank == r0) jsel = j + 1;
-      }
-      jsel = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(jsel));
-      const int j = jsel - 1;
-      const double e = ce[j], f = cf[j];
-      const bool fin = !isinf(e);
-      const Pow2 sc(fin ? -static_cast<int>(e) : 0);
-      const Divisor dv = make_divisor(f);
-      E* ucol = Ag + static_cast<int64_t>(r0) * lda;
-      const E* g = G(mm) + j * mi;
-      for (int i = lane; i < mi; i += 32) {
-        E x = g[i];
-        if (fin) {
-          if constexpr (CPLX) x = make_double2(divide(sc(x.x), dv), divide(sc(x.y), dv));
-          else x = divide(sc(x), dv);
-        }
-        ucol[i] = x;
-      }
-      E* vcol = Vb + static_cast<int64_t>(r0) * ldv;
-      for (int i = lane; i < ni; i += 32) vcol[i] = Vs(mm)[j * ni + i];
-      if (lane == 0) {
-        const double es = fin ? e - s_[mm] : e;
-        sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
-      }
-    }
-    if (threadIdx.x == 0) {
-      if (status_out) status_out[b] = conv[mm] ? JSVD_OK : JSVD_ENOCONV;
-      if (sweeps_out) sweeps_out[b] = sweeps[mm];
-      if (transforms_out) transforms_out[b] = Ttot[mm];
-    }
-    __syncthreads();
-  }
-}
-
-static size_t batched2_smem(bool cplx, int64_t m, int64_t n) {
-  const size_t w = cplx ? 16 : 8;
-  return 2 * w * (m * n + n * n) + sizeof(PairSlot) * 2 * 2 * 16 + 2 * 2 * sizeof(double) * n +
-         2 * (n - 1) * (n / 2);
-}
-
 static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
   const size_t w = cplx ? 16 : 8;
   return w * (m * n + n * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
@@ -815,32 +461,7 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                                            sigma, max_sweeps, sweeps_done, status,
                                                            transforms, Fm, Kr, tol);
   };
-  // two matrices per CTA when a step has at most 16 pairs and both fit
-  const size_t smem2 = batched2_smem(cplx, m, n);
-  const bool two = n <= 32 && batch >= 2 && smem2 <= 220 * 1024;
-  auto go2 = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
-    kern<<<static_cast<unsigned>((batch + 1) / 2), 2 * kBT, smem2, st>>>(
-        batch, m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps, sweeps_done, status,
-        transforms, Fm, Kr, tol);
-  };
-  if (two) {
-    if (cplx) {
-      if (m == 32) go2(batched_svd2_kernel<true, 2, true>);
-      else if (m == 64) go2(batched_svd2_kernel<true, 4, true>);
-      else if (m == 128) go2(batched_svd2_kernel<true, 8, true>);
-      else if (m < 32) go2(batched_svd2_kernel<true, 2, false>);
-      else if (m < 64) go2(batched_svd2_kernel<true, 4, false>);
-      else go2(batched_svd2_kernel<true, 8, false>);
-    } else {
-      if (m == 32) go2(batched_svd2_kernel<false, 2, true>);
-      else if (m == 64) go2(batched_svd2_kernel<false, 4, true>);
-      else if (m == 128) go2(batched_svd2_kernel<false, 8, true>);
-      else if (m < 32) go2(batched_svd2_kernel<false, 2, false>);
-      else if (m < 64) go2(batched_svd2_kernel<false, 4, false>);
-      else go2(batched_svd2_kernel<false, 8, false>);
-    }
-  } else if (cplx) {
+  if (cplx) {
     if (m == 32) go(batched_svd_kernel<true, 2, true>);
     else if (m == 64) go(batched_svd_kernel<true, 4, true>);
     else if (m == 128) go(batched_svd_kernel<true, 8, true>);
