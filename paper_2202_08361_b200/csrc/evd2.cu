@@ -99,6 +99,11 @@ __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+  // programmatic dependent launch: the next grid in the stream may be scheduled
+  // into the SMs this grid's last wave leaves free; every grid waits for its
+  // predecessor's completion (and memory) before touching data
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   evd2_chunk<CPLX, TAN, NOBACK>(blockIdx.x, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
 }
 
@@ -138,8 +143,17 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     // one 512-matrix chunk per CTA: the measured-best shape for both configs
     // (a persistent grid-stride variant was slower for configs[0] and [1])
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
-    evd2_vec2_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(chunks), threads, 0, st>>>(
-        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(chunks));
+    cfg.blockDim = dim3(threads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK>, r, a11, a22, re, im, l1, l2, c,
+                       sr, si, zeta, perm);
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
