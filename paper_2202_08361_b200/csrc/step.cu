@@ -63,6 +63,11 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   const auto sP = [&](int j) -> E& { return sx[(2 * j) * T + threadIdx.x]; };
   const auto sQ = [&](int j) -> E& { return sx[(2 * j + 1) * T + threadIdx.x]; };
 
+  // programmatic dependent launch: the next step's CTAs may be scheduled into
+  // the SMs this step's last wave frees; no global data is touched before the
+  // previous step has completed and its memory is visible
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int crank = CL > 1 ? static_cast<int>(blockIdx.x % CL) : 0;
   const int64_t pair = blockIdx.x / CL;
   if constexpr (CL > 1) {  // the DSMEM rounds' mbarriers (published before any push)
@@ -464,19 +469,28 @@ static void mark_attrs_done(const void* k) {
 
 template <typename Kern, typename... Args>
 static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, cudaStream_t st,
-                             Args... args) {
+                             bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CL > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CL;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = CL > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   // kernel attributes are set once per kernel (not inside a CUDA-graph capture
   // of later launches)
   if ((CL > 8 || smem > 48 * 1024) && !attrs_done(reinterpret_cast<const void*>(k))) {
@@ -508,16 +522,16 @@ static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams&
   const size_t sm = static_cast<size_t>(NSs) * 2 * 256 * sizeof(E);
   if (g.NS) {
     switch (g.CL) {
-      case 8: return launch_cl(step_kernel<CPLX, 256, 8, NRr, NSs>, grid, 256, 8, sm, st, P);
-      case 16: return launch_cl(step_kernel<CPLX, 256, 16, NRr, NSs>, grid, 256, 16, sm, st, P);
+      case 8: return launch_cl(step_kernel<CPLX, 256, 8, NRr, NSs>, grid, 256, 8, sm, st, true, P);
+      case 16: return launch_cl(step_kernel<CPLX, 256, 16, NRr, NSs>, grid, 256, 16, sm, st, true, P);
     }
     return cudaErrorInvalidValue;
   }
   switch (g.CL) {
-    case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR, 0>, grid, 256, 1, 0, st, P);
-    case 2: return launch_cl(step_kernel<CPLX, 256, 2, NR, 0>, grid, 256, 2, 0, st, P);
-    case 4: return launch_cl(step_kernel<CPLX, 256, 4, NR, 0>, grid, 256, 4, 0, st, P);
-    case 8: return launch_cl(step_kernel<CPLX, 256, 8, NR, 0>, grid, 256, 8, 0, st, P);
+    case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR, 0>, grid, 256, 1, 0, st, true, P);
+    case 2: return launch_cl(step_kernel<CPLX, 256, 2, NR, 0>, grid, 256, 2, 0, st, true, P);
+    case 4: return launch_cl(step_kernel<CPLX, 256, 4, NR, 0>, grid, 256, 4, 0, st, true, P);
+    case 8: return launch_cl(step_kernel<CPLX, 256, 8, NR, 0>, grid, 256, 8, 0, st, true, P);
   }
   return cudaErrorInvalidValue;
 }
@@ -536,16 +550,16 @@ static cudaError_t launch_colnorm_t(const Geo& g, int64_t m, int64_t n, const do
   const int64_t grid = n * g.CL;
   if (g.NS) {
     switch (g.CL) {
-      case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, 2 * NR>, grid, 256, 8, 0, st, m, G, ldg, ce, cf);
-      case 16: return launch_cl(colnorm_kernel<CPLX, 256, 16, 2 * NR>, grid, 256, 16, 0, st, m, G, ldg, ce, cf);
+      case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, 2 * NR>, grid, 256, 8, 0, st, false, m, G, ldg, ce, cf);
+      case 16: return launch_cl(colnorm_kernel<CPLX, 256, 16, 2 * NR>, grid, 256, 16, 0, st, false, m, G, ldg, ce, cf);
     }
     return cudaErrorInvalidValue;
   }
   switch (g.CL) {
-    case 1: return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, 0, st, m, G, ldg, ce, cf);
-    case 2: return launch_cl(colnorm_kernel<CPLX, 256, 2, NR>, grid, 256, 2, 0, st, m, G, ldg, ce, cf);
-    case 4: return launch_cl(colnorm_kernel<CPLX, 256, 4, NR>, grid, 256, 4, 0, st, m, G, ldg, ce, cf);
-    case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, NR>, grid, 256, 8, 0, st, m, G, ldg, ce, cf);
+    case 1: return launch_cl(colnorm_kernel<CPLX, 256, 1, NR>, grid, 256, 1, 0, st, false, m, G, ldg, ce, cf);
+    case 2: return launch_cl(colnorm_kernel<CPLX, 256, 2, NR>, grid, 256, 2, 0, st, false, m, G, ldg, ce, cf);
+    case 4: return launch_cl(colnorm_kernel<CPLX, 256, 4, NR>, grid, 256, 4, 0, st, false, m, G, ldg, ce, cf);
+    case 8: return launch_cl(colnorm_kernel<CPLX, 256, 8, NR>, grid, 256, 8, 0, st, false, m, G, ldg, ce, cf);
   }
   return cudaErrorInvalidValue;
 }
