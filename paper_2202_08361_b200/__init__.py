@@ -20,7 +20,8 @@ import torch
 from ._build import LIB
 
 __all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
-           "gesvj_workspace", "gesvj_batched", "launch_count", "JsvdError", "R64", "C64",
+           "gesvj_workspace", "gesvj_batched", "launch_count", "evd2_batched_host",
+           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
 R64, C64, R32, C32 = 0, 1, 2, 3
@@ -69,6 +70,17 @@ def lib():
         L.jsvd_gesvj_batched.restype = ct.c_int
         L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
                                          _i64, _vp, _i32, _vp, _vp, _vp, _vp]
+        L.jsvd_evd2_host_workspace.restype = ct.c_int
+        L.jsvd_evd2_host_workspace.argtypes = [ct.c_int, _i64, ct.POINTER(ct.c_size_t)]
+        L.jsvd_evd2_batched_host.restype = ct.c_int
+        L.jsvd_evd2_batched_host.argtypes = ([ct.c_int, _i64] + [_vp] * 11 +
+                                             [ct.c_uint32, _i64, _vp, ct.c_size_t, _vp])
+        L.jsvd_gesvj_batched_host_workspace.restype = ct.c_int
+        L.jsvd_gesvj_batched_host_workspace.argtypes = [ct.c_int, _i64, _i64, _i64,
+                                                        ct.POINTER(ct.c_size_t)]
+        L.jsvd_gesvj_batched_host.restype = ct.c_int
+        L.jsvd_gesvj_batched_host.argtypes = ([ct.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
+                                               _vp, _vp, _vp, _i64, _vp, ct.c_size_t, _vp])
         L.jsvd_fp64_peak.restype = ct.c_int
         L.jsvd_fp64_peak.argtypes = [_i32, _i64, _vp, ct.POINTER(_i64), _vp]
         L.jsvd_maxnorm.restype = ct.c_int
@@ -153,6 +165,102 @@ def evd2_batched(a11, a22, a21_re, a21_im=None, flags=0, out=None, stream=None):
             _p(out["lam2"]), _p(out["cos"]), _p(out["sin_re"]), _p(out.get("sin_im")),
             _p(out.get("zeta")), _p(out.get("perm")), flags, _stream(stream))
     _check(st, name)
+    return out
+
+
+def _host(t, name, dtype):
+    if t is None:
+        return None
+    if t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} HOST tensor (pinned for overlap)")
+    return ct.c_void_p(t.data_ptr())
+
+
+def evd2_host_workspace(dtype, cplx, chunk):
+    b = ct.c_size_t()
+    code = (C64 if cplx else R64) if dtype == torch.float64 else (C32 if cplx else R32)
+    _check(lib().jsvd_evd2_host_workspace(code, chunk, ct.byref(b)), "jsvd_evd2_host_workspace")
+    return b.value
+
+
+def evd2_batched_host(a11, a22, a21_re, a21_im=None, flags=0, out=None, chunk=1 << 21,
+                      work=None, stream=None):
+    """evd2_batched on HOST tensors (jsvd_evd2_batched_host): chunked H2D /
+    kernel / D2H pipelined over three internal streams.  Inputs and ``out``
+    (same keys as evd2_batched; allocated pinned when None) live in host memory;
+    ``work`` is a uint8 CUDA tensor of at least evd2_host_workspace() bytes.
+    Asynchronous on ``stream``: synchronise it before reading ``out``."""
+    cplx = a21_im is not None
+    r, dt = a11.numel(), a11.dtype
+    if dt not in (torch.float64, torch.float32):
+        raise ValueError("a11 must be float64 or float32")
+    if out is None:
+        out = {k: torch.empty(r, dtype=dt, pin_memory=True) for k in ("lam1", "lam2", "cos", "sin_re")}
+        out["sin_im"] = torch.empty(r, dtype=dt, pin_memory=True) if cplx else None
+        out["zeta"] = torch.empty(r, dtype=torch.int32, pin_memory=True)
+        out["perm"] = torch.empty((r + 31) // 32, dtype=torch.int32, pin_memory=True)
+    ptrs = []
+    for n_, t in (("a11", a11), ("a22", a22), ("a21_re", a21_re), ("a21_im", a21_im),
+                  ("lam1", out["lam1"]), ("lam2", out["lam2"]), ("cos", out["cos"]),
+                  ("sin_re", out["sin_re"]), ("sin_im", out.get("sin_im"))):
+        if t is not None and t.numel() != r:
+            raise ValueError(f"{n_} must have length {r}")
+        ptrs.append(_host(t, n_, dt))
+    ptrs.append(_host(out.get("zeta"), "zeta", torch.int32))
+    ptrs.append(_host(out.get("perm"), "perm", torch.int32))
+    wb = evd2_host_workspace(dt, cplx, chunk)
+    if work is None:
+        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    if not work.is_cuda or work.numel() < wb:
+        raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
+    code = (C64 if cplx else R64) if dt == torch.float64 else (C32 if cplx else R32)
+    st = lib().jsvd_evd2_batched_host(code, r, *ptrs, flags, chunk, _p(work), work.numel(),
+                                      _stream(stream))
+    _check(st, "jsvd_evd2_batched_host")
+    return out
+
+
+def gesvj_batched_host_workspace(cplx, m, n, chunk):
+    b = ct.c_size_t()
+    _check(lib().jsvd_gesvj_batched_host_workspace(C64 if cplx else R64, m, n, chunk, ct.byref(b)),
+           "jsvd_gesvj_batched_host_workspace")
+    return b.value
+
+
+def gesvj_batched_host(A, max_sweeps=30, out=None, chunk=4096, work=None, stream=None,
+                       transforms=True):
+    """gesvj_batched on HOST tensors (jsvd_gesvj_batched_host).  A: (batch, m, n)
+    host tensor whose matrices are packed column-major (A.stride() == (m*n, 1, m));
+    A is not modified.  Returns dict(U, V, sigma, sweeps, status[, transforms]) of
+    host tensors (pinned when allocated here).  Asynchronous on ``stream``."""
+    b, m, n = A.shape
+    if A.dtype not in (torch.float64, torch.complex128) or A.is_cuda or \
+            A.stride() != (m * n, 1, m):
+        raise ValueError("A must be a host float64/complex128 tensor of packed column-major matrices")
+    cplx = A.dtype == torch.complex128
+    if out is None:
+        out = dict(U=torch.empty((b, n, m), dtype=A.dtype, pin_memory=True).transpose(1, 2),
+                   V=torch.empty((b, n, n), dtype=A.dtype, pin_memory=True).transpose(1, 2),
+                   sigma=torch.empty((b, n), dtype=torch.float64, pin_memory=True),
+                   sweeps=torch.empty(b, dtype=torch.int32, pin_memory=True),
+                   status=torch.empty(b, dtype=torch.int32, pin_memory=True),
+                   transforms=torch.empty(b, dtype=torch.int64, pin_memory=True) if transforms else None)
+    for k, shp in (("U", (m * n, 1, m)), ("V", (n * n, 1, n))):
+        if out[k].is_cuda or out[k].dtype != A.dtype or out[k].stride() != shp or \
+                out[k].shape != (b, shp[2], n):
+            raise ValueError(f"out[{k!r}] must be a host tensor of packed column-major matrices")
+    wb = gesvj_batched_host_workspace(cplx, m, n, chunk)
+    if work is None:
+        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    if not work.is_cuda or work.numel() < wb:
+        raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
+    st = lib().jsvd_gesvj_batched_host(
+        C64 if cplx else R64, b, m, n, ct.c_void_p(A.data_ptr()), ct.c_void_p(out["U"].data_ptr()),
+        ct.c_void_p(out["V"].data_ptr()), _host(out["sigma"], "sigma", torch.float64), max_sweeps,
+        _host(out.get("sweeps"), "sweeps", torch.int32), _host(out.get("status"), "status", torch.int32),
+        _host(out.get("transforms"), "transforms", torch.int64), chunk, _p(work), work.numel(),
+        _stream(stream))
+    _check(st, "jsvd_gesvj_batched_host")
     return out
 
 
