@@ -2,12 +2,16 @@
 // SVDs (BASELINE configs[3]: 65536 complex 64 x 32), one CTA per matrix, the
 // whole iteration (G and V) resident in shared memory: HBM is touched once to
 // load A and once to store U, V, sigma.  Same arithmetic as jsvd_gesvj with
-// nblocks = n (flat round-robin) and the reduction spec R = (16, 1, [8,4,2,1]):
-// lane L of a HALF-warp owns rows L, L+16, ... of a pair, so one warp serves
-// two pairs at once and every shuffle of a reduction serves both.
+// nblocks = n (flat round-robin) and the reduction spec R = (W, 1, [W/2..1]),
+// W = 8 for m <= 64 (16 above): lane L of a W-lane group owns rows L, L+W, ...
+// of a pair, so one warp serves 32/W pairs at once and every shuffle of a
+// reduction serves all of them.  W = 8 (128 threads, 8 rows per lane for
+// configs[3]) issues ~30% fewer instructions per step than W = 16: the
+// shuffle trees are one level shorter and the per-group overhead is spread
+// over twice the rows.
 //
-// Per step (n/2 pairs; 256 threads = 16 half-warps):
-//   A  every half-warp, one pair: exponent max, SSQ of x 2^-E (R#14) and the
+// Per step (n/2 pairs; 16 W threads = 16 lane groups):
+//   A  every lane group, one pair: exponent max, SSQ of x 2^-E (R#14) and the
 //      dot of the columns prescaled by 2^-e (Alg 3.1) -- only the vector work
 //      and the sums; the per-pair scalar tail goes to B
 //   B  warp 0, ONE LANE PER PAIR: f = sqrt(g), the division of the dot, the
@@ -15,20 +19,20 @@
 //      every transformed pair -- the batch of EVDs of Alg 4.1 line 26
 //      vectorised across lanes as the paper vectorises it across SIMD lanes
 //
-//   C  every half-warp, one pair: rotation of its G and V columns (Alg 3.4);
+//   C  every lane group, one pair: rotation of its G and V columns (Alg 3.4);
 //      M-tilde tracked by its high word (only floor(lg M-tilde) enters Eq. skr)
 // The Eq. (skr) rescale check runs at every step (flat round-robin, R#21).
 #include <cmath>
+#include <type_traits>
 
 #include "jsvd_host.h"
 #include "step_dev.cuh"
 
 namespace jsvd {
 
-constexpr int kBT = 256;  // threads per CTA (8 warps, 16 half-warps)
-constexpr int kBNW = kBT / 32;
-constexpr int kBNH = kBT / 16;
-constexpr int kBW = 16;  // lanes per pair (R.W)
+// W lanes per pair (R.W = 8 for m <= 64, 16 above) and 16 lane groups per CTA
+// (16 W threads): one pass of phases A and C covers the 16 pairs of n = 32
+constexpr int kBNH = 16;
 
 struct PairSlot {
   double ar, ai;  // sums of the prescaled dot (Alg 3.1 lines 5-6)
@@ -39,28 +43,31 @@ struct PairSlot {
   int pad;
 };
 
-// sum over the 16 lanes of each half-warp, xor offsets 8, 4, 2, 1 (R)
+// sum over the W lanes of each lane group, xor offsets W/2, ..., 1 (R)
+template <int W>
 __device__ __forceinline__ double hsum(double v) {
 #pragma unroll
-  for (int o = 8; o >= 1; o /= 2) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = W / 2; o >= 1; o /= 2) v = v + __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+template <int W>
 __device__ __forceinline__ uint32_t hmax_u32(uint32_t v) {
 #pragma unroll
-  for (int o = 8; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = W / 2; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+template <int W>
 __device__ __forceinline__ uint64_t hmax_u64(uint64_t v) {
 #pragma unroll
-  for (int o = 8; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = W / 2; o >= 1; o /= 2) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
 
-// floor(lg max|component|) over the half-warp's column slice x[0..NR):
+// floor(lg max|component|) over the lane group's column slice x[0..NR):
 // from the high words; a column whose largest component is subnormal (or zero)
 // takes the exact 64-bit path (warp-uniform branch).  kIntMin: zero column.
-template <int NR, typename E>
+template <int NR, int W, typename E>
 __device__ __forceinline__ void col_exponents(const E* xp, const E* xq, int& Ep, int& Eq) {
   uint32_t hp = 0, hq = 0;
 #pragma unroll
@@ -68,8 +75,8 @@ __device__ __forceinline__ void col_exponents(const E* xp, const E* xq, int& Ep,
     hp = hi_max(xp[j], hp);
     hq = hi_max(xq[j], hq);
   }
-  hp = hmax_u32(hp);
-  hq = hmax_u32(hq);
+  hp = hmax_u32<W>(hp);
+  hq = hmax_u32<W>(hq);
   Ep = static_cast<int>(hp >> 20) - 1023;
   Eq = static_cast<int>(hq >> 20) - 1023;
   if (__any_sync(0xffffffffu, hp < 0x00100000u || hq < 0x00100000u)) {
@@ -79,8 +86,8 @@ __device__ __forceinline__ void col_exponents(const E* xp, const E* xq, int& Ep,
       mp = absmax_bits(xp[j], mp);
       mq = absmax_bits(xq[j], mq);
     }
-    mp = hmax_u64(mp);
-    mq = hmax_u64(mq);
+    mp = hmax_u64<W>(mp);
+    mq = hmax_u64<W>(mq);
     if (hp < 0x00100000u) Ep = ilogb_or_min(mp);
     if (hq < 0x00100000u) Eq = ilogb_or_min(mq);
   }
@@ -99,13 +106,14 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
   e = E + k / 2;
 }
 
-// FULL: m == 16 NR (configs[3]: 64 = 16 x 4), so no row needs a bounds check
-template <bool CPLX, int NR, bool FULL>
-__global__ void __launch_bounds__(kBT) batched_svd_kernel(
+// FULL: m == W NR (configs[3]: 64 = 8 x 8), so no row needs a bounds check
+template <bool CPLX, int NR, bool FULL, int W>
+__global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
     int64_t* transforms_out, int Fm, int Kr, double tol) {
   using E = typename Elem<CPLX>::T;
+  constexpr int kBT = kBNH * W, kBNW = kBT / 32, kBW = W, kGPW = 32 / W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* sG = reinterpret_cast<E*>(smem_raw);
   E* sV = sG + m * n;
@@ -122,7 +130,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   E* Ag = reinterpret_cast<E*>(A) + b * strideA;
   E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4;
+  const int hl = threadIdx.x & (W - 1), hw = threadIdx.x / W;
   const int np = static_cast<int>(n / 2);
   const int mi = static_cast<int>(m), ni = static_cast<int>(n);
   // the flat round-robin ordering (R#20), once per CTA
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           __syncthreads();
         }
       }
-      // ---- phase A: half-warp per pair: exponent max, SSQ, prescaled dot
+      // ---- phase A: lane group per pair: exponent max, SSQ, prescaled dot
       for (int l0 = 0; l0 < np; l0 += kBNH) {  // uniform trip count: both halves shuffle
         const int l = l0 + hw;
         const bool act = l < np;
@@ -235,11 +243,11 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           xq[j] = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
         }
         int Ep, Eq;
-        col_exponents<NR>(xp, xq, Ep, Eq);
+        col_exponents<NR, W>(xp, xq, Ep, Eq);
         double sp = Ep != kIntMin ? ssq_lane<NR>(xp, Ep) : 0.0;
         double sq = Eq != kIntMin ? ssq_lane<NR>(xq, Eq) : 0.0;
-        sp = hsum(sp);
-        sq = hsum(sq);
+        sp = hsum<W>(sp);
+        sq = hsum<W>(sq);
         int ep = kIntMin, eq = kIntMin;
         double gpv = 1.0, gqv = 1.0;
         if (Ep != kIntMin) eg_from_ssq(Ep, sp, ep, gpv);
@@ -247,8 +255,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
         const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19
         double ar = 0.0, ai = 0.0;
         if (!zero_col) dot_lane<NR>(xq, xp, eq, ep, ar, ai);
-        ar = hsum(ar);
-        if (CPLX) ai = hsum(ai);
+        ar = hsum<W>(ar);
+        if (CPLX) ai = hsum<W>(ai);
         if (act && hl == 0) {
           PairSlot& sl = slots[l];
           sl.ar = zero_col ? 0.0 : ar;
@@ -293,8 +301,8 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
           tcount += __popc(__ballot_sync(0xffffffffu, tr));
         }
         if (lane == 0) sT += tcount;
-      } else if (pend_k >= 0) {  // half-warps 2..15: V of the previous step
-        rotate_v(slots2 + pend_buf * np, pend_k, hw - 2, kBNH - 2, hl, kBW);
+      } else if (pend_k >= 0) {  // the lane groups of warps 1..: V of the previous step
+        rotate_v(slots2 + pend_buf * np, pend_k, hw - kGPW, kBNH - kGPW, hl, kBW);
       }
       __syncthreads();
       // ---- phase C: rotations of G (Alg 3.4), M-tilde
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   }
   // ---- finalize: norms with the step's R (R#23),
   // U = G diag(2^-e / f), sigma, sort
-  for (int j0 = 0; j0 < ni; j0 += kBNH) {  // half-warp per column, uniform trip count
+  for (int j0 = 0; j0 < ni; j0 += kBNH) {  // lane group per column, uniform trip count
     const int j = j0 + hw;
     const bool act = j < ni;
     const E* g = sG + (act ? j : 0) * mi;
@@ -358,7 +366,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       x[jj] = (FULL || i < mi) ? g[i] : Elem<CPLX>::zero();
       mj = absmax_bits(x[jj], mj);
     }
-    mj = hmax_u64(mj);
+    mj = hmax_u64<W>(mj);
     const int Ej = ilogb_or_min(mj);
     double sj = 0.0;
     if (Ej != kIntMin) {
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
       for (int jj = 0; jj < NR; ++jj)
         if (FULL || jj * kBW + hl < mi) sj = ssq_acc(f(x[jj]), sj);
     }
-    sj = hsum(sj);
+    sj = hsum<W>(sj);
     double e = -INFINITY, f = 1.0;
     if (Ej != kIntMin) ef_from_ssq(Ej, sj, e, f);
     if (act && hl == 0) {
@@ -418,6 +426,9 @@ __global__ void __launch_bounds__(kBT) batched_svd_kernel(
   }
 }
 
+// lanes per pair of the kernel jsvd_gesvj_batched launches for m (R.W)
+static int batched_w(int64_t m) { return m <= 64 ? 8 : 16; }
+
 static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
   const size_t w = cplx ? 16 : 8;
   return w * (m * n + n * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
@@ -455,27 +466,24 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
   const int Fm = Fm_host(cplx, m), Kr = cplx ? 1020 : 1022;
   const double tol = std::ldexp(std::sqrt(static_cast<double>(m)), -53);
   cudaError_t e;
-  auto go = [&](auto kern) {
+  auto go = [&](auto kern, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<static_cast<unsigned>(batch), kBT, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
-                                                           sigma, max_sweeps, sweeps_done, status,
-                                                           transforms, Fm, Kr, tol);
+    kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
+                                                              sigma, max_sweeps, sweeps_done, status,
+                                                              transforms, Fm, Kr, tol);
   };
-  if (cplx) {
-    if (m == 32) go(batched_svd_kernel<true, 2, true>);
-    else if (m == 64) go(batched_svd_kernel<true, 4, true>);
-    else if (m == 128) go(batched_svd_kernel<true, 8, true>);
-    else if (m < 32) go(batched_svd_kernel<true, 2, false>);
-    else if (m < 64) go(batched_svd_kernel<true, 4, false>);
-    else go(batched_svd_kernel<true, 8, false>);
-  } else {
-    if (m == 32) go(batched_svd_kernel<false, 2, true>);
-    else if (m == 64) go(batched_svd_kernel<false, 4, true>);
-    else if (m == 128) go(batched_svd_kernel<false, 8, true>);
-    else if (m < 32) go(batched_svd_kernel<false, 2, false>);
-    else if (m < 64) go(batched_svd_kernel<false, 4, false>);
-    else go(batched_svd_kernel<false, 8, false>);
-  }
+  // W = batched_w(m) lanes per pair; NR = rows per lane
+  auto pick = [&](auto cplx_t) {
+    constexpr bool C = decltype(cplx_t)::value;
+    if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
+    else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);
+    else if (m < 64) go(batched_svd_kernel<C, 8, false, 8>, 128);
+    else if (m == 128) go(batched_svd_kernel<C, 8, true, 16>, 256);
+    else go(batched_svd_kernel<C, 8, false, 16>, 256);
+  };
+  if (cplx) pick(std::true_type{});
+  else pick(std::false_type{});
   note_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
@@ -485,10 +493,10 @@ extern "C" jsvd_status jsvd_batched_rspec(jsvd_dtype dt, int64_t m, int32_t* W, 
                                           int32_t* offs, int32_t* noffs) {
   if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || m > 128 || !W || !c || !offs || !noffs)
     return JSVD_EINVAL;
-  *W = kBW;
+  *W = batched_w(m);
   *c = 1;
   int k = 0;
-  for (int o = kBW / 2; o >= 1; o /= 2) offs[k++] = o;
+  for (int o = *W / 2; o >= 1; o /= 2) offs[k++] = o;
   *noffs = k;
   return JSVD_OK;
 }
