@@ -108,7 +108,7 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
 
 // FULL: m == W NR (configs[3]: 64 = 8 x 8), so no row needs a bounds check
 template <bool CPLX, int NR, bool FULL, int W>
-__global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
+__global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
     int64_t* transforms_out, int Fm, int Kr, double tol) {
@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
   constexpr int kBT = kBNH * W, kBNW = kBT / 32, kBW = W, kGPW = 32 / W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   E* sG = reinterpret_cast<E*>(smem_raw);
-  E* sV = sG + m * n;
-  PairSlot* slots2 = reinterpret_cast<PairSlot*>(sV + n * n);  // [2][n/2]: steps alternate
+  // V lives in global memory, in the matrix's own A storage (free once A is in
+  // shared memory; V(i, j) at Ag[j lda + i], n <= m <= lda): shared memory then
+  // holds only G, so 5 CTAs fit per SM.  V is touched only by the rotations in
+  // phase B's shadow, where its L1/L2 latency is hidden.
+  PairSlot* slots2 = reinterpret_cast<PairSlot*>(sG + m * n);  // [2][n/2]: steps alternate
   double* ce = reinterpret_cast<double*>(slots2 + n);
   double* cf = ce + n;
   uint8_t* sPairs = reinterpret_cast<uint8_t*>(cf + n);  // (n-1) x n/2 pivot pairs (n <= 64)
@@ -125,6 +128,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
   __shared__ uint32_t sMt;  // high word of M-tilde (its floor(lg) is all Eq. skr uses)
   __shared__ int sT;
   __shared__ uint64_t wred[kBNW];
+  __shared__ int sSel[64];  // finalize: input column of each output rank
 
   const int64_t b = blockIdx.x;
   E* Ag = reinterpret_cast<E*>(A) + b * strideA;
@@ -154,11 +158,6 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
       mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
     }
   }
-  for (int k = threadIdx.x; k < ni * ni; k += kBT) {
-    const int j = k / ni, i = k - j * ni;
-    if constexpr (CPLX) sV[k] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    else sV[k] = i == j ? 1.0 : 0.0;
-  }
   {
     const uint64_t M0 = cta_max_u64<kBT>(mx, wred);
     if (threadIdx.x == 0) sM0 = M0;
@@ -180,9 +179,16 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
     else sG[k] = scalbn_rn(sG[k], s);
   }
   if (threadIdx.x == 0) sMt = hi32(scalbn_rn(M0, s));
+  // V = I over A's storage (every read of A above precedes the barrier in
+  // cta_max_u64)
+  for (int k = threadIdx.x; k < ni * ni; k += kBT) {
+    const int j = k / ni, i = k - j * ni;
+    if constexpr (CPLX) Ag[static_cast<int64_t>(j) * lda + i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    else Ag[static_cast<int64_t>(j) * lda + i] = i == j ? 1.0 : 0.0;
+  }
   __syncthreads();
 
-  // V of step k is rotated by warps 1..7 while warp 0 runs phase B of step
+  // V of step k is rotated by warps 1.. while warp 0 runs phase B of step
   // k+1 (V never enters a decision, Alg 3.4 applies the same (c, C, S) to it);
   // the slots of consecutive steps alternate between two buffers
   const auto rotate_v = [&](const PairSlot* sl_, int kstep, int l_begin, int l_step, int lane0,
@@ -191,8 +197,10 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
       const PairSlot& sl = sl_[l];
       if (!sl.transform) continue;
       const int p = sPairs[2 * (kstep * np + l)], q = sPairs[2 * (kstep * np + l) + 1];
-      E* vp = sV + p * ni;
-      E* vq = sV + q * ni;
+      E* vp = Ag + static_cast<int64_t>(p) * lda;
+      E* vq = Ag + static_cast<int64_t>(q) * lda;
+      // one row at a time: prefetching rows costs registers, and at the
+      // 96-register cap of 5 CTAs per SM any spill costs more than it hides
       for (int i = lane0; i < ni; i += lanes) {
         E a = vp[i], bq = vq[i];
         rot_elem(a, bq, sl.c, sl.C, sl.S);
@@ -398,6 +406,21 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
     }
     jsel = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(jsel));
     const int j = jsel - 1;
+    if (lane == 0) sSel[r0] = j;
+    // V's output column r0 from the working V in A's storage
+    E* vcol = Vb + static_cast<int64_t>(r0) * ldv;
+    const E* vw = Ag + static_cast<int64_t>(j) * lda;
+    for (int i = lane; i < ni; i += 32) vcol[i] = vw[i];
+    if (lane == 0) {
+      const double e = ce[j], f = cf[j];
+      const bool fin = !isinf(e);
+      const double es = fin ? e - s : e;
+      sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
+    }
+  }
+  __syncthreads();  // every read of the working V precedes the writes of U over it
+  for (int r0 = warp; r0 < ni; r0 += kBNW) {
+    const int j = sSel[r0];
     const double e = ce[j], f = cf[j];
     const bool fin = !isinf(e);
     const Pow2 sc(fin ? -static_cast<int>(e) : 0);
@@ -412,12 +435,6 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 4 : 2) batched_svd_kernel(
       }
       ucol[i] = x;
     }
-    E* vcol = Vb + static_cast<int64_t>(r0) * ldv;
-    for (int i = lane; i < ni; i += 32) vcol[i] = sV[j * ni + i];
-    if (lane == 0) {
-      const double es = fin ? e - s : e;
-      sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
-    }
   }
   if (threadIdx.x == 0) {
     if (status_out) status_out[b] = converged ? JSVD_OK : JSVD_ENOCONV;
@@ -431,7 +448,7 @@ static int batched_w(int64_t m) { return m <= 64 ? 8 : 16; }
 
 static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
   const size_t w = cplx ? 16 : 8;
-  return w * (m * n + n * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
+  return w * (m * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
          2 * (n - 1) * (n / 2);
 }
 
