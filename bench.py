@@ -153,7 +153,7 @@ class EvdWorkload:
         self.dev, self.out = self.sets[0]
         self.k = 0
         self.units_per_step = self.r
-        self.kernel = "evd2f_vec4_kernel" if self.f32 else "evd2_vec2_kernel"
+        self.kernel = "evd2f_vec4_kernel" if self.f32 else ("evd2_vec2_kernel" if self.cplx else "evd2_scalar_kernel")
         self.l2_note = ("inputs+outputs %.1f GB per step > 126 MB L2 (no flush needed)"
                         % (self.unit_bytes * self.r / 1e9)) if self.cplx else \
             "63 MB per step; steps cycle through 4 input/output sets (252 MB > 126 MB L2)"
@@ -714,6 +714,8 @@ def run_jsvd(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
                 "peak_source": peak_src, "kernel": wl.kernel}
+    if isinstance(wl, EvdWorkload):
+        extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
     if isinstance(wl, GesvjWorkload):
         extra.update(extra_g)
         s = wl.last["sigma"].cpu().numpy()
@@ -780,6 +782,37 @@ def run_jsvd(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def size_matched_copy(wl, steps, peak):
+    """Context for the EVD's roofline fraction: a plain device copy (torch
+    copy_, read B/2 + write B/2 bytes per step, B = the EVD's algorithmic bytes)
+    cycling the same number of buffer sets, K steps in one CUDA graph -- what a
+    trivially memory-bound launch of this size reaches on this GPU."""
+    import torch
+    half = int(wl.bytes_per_step() // 2) // 8
+    sets = [(torch.empty(half, dtype=torch.float64, device="cuda").fill_(1.0),
+             torch.empty(half, dtype=torch.float64, device="cuda")) for _ in range(wl.nsets)]
+    for s_, d_ in sets:
+        d_.copy_(s_)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k in range(steps):
+            d_, s_ = sets[k % len(sets)][1], sets[k % len(sets)][0]
+            for o in range(0, half, 1 << 27):  # <= 1 GiB slices: 32-bit-indexed copy kernels
+                d_[o:o + (1 << 27)].copy_(s_[o:o + (1 << 27)])
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    ach = 2 * half * 8 / (ms / 1e3) / 1e9
+    del sets, g
+    torch.cuda.empty_cache()
+    return {"achieved": ach, "frac": ach / peak, "ms_per_step": ms,
+            "what": "torch copy_ of the same bytes (read B/2 + write B/2), same buffer-set cycling"}
 
 
 def run_reference(args):
