@@ -231,6 +231,10 @@ extern "C" jsvd_status jsvd_evd2_batched(jsvd_dtype dt, int64_t r, const double*
   if (zeta && !aligned(zeta, 8)) vec = false;
   if (perm && !aligned(perm, 4)) return JSVD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (debug_enabled()) {
+    const jsvd_status ds = debug_check_finite<double>(r, a11, a22, a21_re, a21_im, st);
+    if (ds != JSVD_OK) return ds;
+  }
   cudaError_t e = cplx ? dispatch_flags<true>(flags, vec, r, a11, a22, a21_re, a21_im, lam1, lam2,
                                               cos_phi, sin_re, sin_im, zeta, perm, st)
                        : dispatch_flags<false>(flags, vec, r, a11, a22, a21_re, nullptr, lam1,

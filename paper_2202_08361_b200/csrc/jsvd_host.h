@@ -9,4 +9,9 @@
 namespace jsvd {
 extern std::atomic<int64_t> g_launches;
 inline void note_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+// JSVD_DEBUG=1 (api.cu): scan EVD inputs for Inf/NaN, synchronously
+bool debug_enabled();
+template <typename T>
+jsvd_status debug_check_finite(int64_t r, const T* a, const T* b, const T* c, const T* d,
+                               cudaStream_t st);
 }  // namespace jsvd

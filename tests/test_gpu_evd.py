@@ -174,3 +174,30 @@ def test_real_full_exponent_range_bitwise(J):
     arrs = (np.concatenate([a11, d]), np.concatenate([a22, d2]), np.concatenate([re, off]))
     for flags in (0, 3):
         _compare(_run(J, arrs, flags), _ref(arrs, flags), False)
+
+
+@pytest.mark.parametrize("f32", [False, True])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_debug_env_reports_nonfinite(J, monkeypatch, f32, cplx):
+    # JSVD_DEBUG=1: Inf/NaN inputs -> JSVD_ENONFINITE, finite inputs unaffected
+    dt = torch.float32 if f32 else torch.float64
+    r = 1000
+    gen = (synth.evd_cfg2_f32 if cplx else synth.evd_cfg1_f32) if f32 else \
+        (synth.evd_cfg2 if cplx else synth.evd_cfg1)
+    a = [torch.from_numpy(x).to(device="cuda", dtype=dt) for x in gen(r)]
+    monkeypatch.setenv("JSVD_DEBUG", "1")
+    ok = J.evd2_batched(*a)
+    torch.cuda.synchronize()
+    ref = J.evd2_batched(*[x.clone() for x in a])  # same finite data: same result
+    assert torch.equal(ok["cos"], ref["cos"])
+    for k, bad in ((0, float("nan")), (len(a) - 1, float("inf"))):
+        b = [x.clone() for x in a]
+        b[k][r - 1] = bad
+        with pytest.raises(J.JsvdError) as ei:
+            J.evd2_batched(*b)
+        assert ei.value.status == -2
+    monkeypatch.delenv("JSVD_DEBUG")
+    b = [x.clone() for x in a]
+    b[0][5] = float("nan")
+    J.evd2_batched(*b)  # no check without the flag (the paper's precondition)
+    torch.cuda.synchronize()
