@@ -714,7 +714,7 @@ def run_jsvd(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
                 "peak_source": peak_src, "kernel": wl.kernel}
-    if isinstance(wl, EvdWorkload):
+    if isinstance(wl, EvdWorkload) and wl.nsets > 1:  # the short configs[0] launch
         extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
     if isinstance(wl, GesvjWorkload):
         extra.update(extra_g)
