@@ -736,3 +736,130 @@ int orc_num_threads(void)
   return 1;
 #endif
 }
+
+/* ======================================================================
+ * NEXT-3: the one-pass "(e, f)" Frobenius norm of Alg SM6.3,
+ * with s lanes, statement by statement.  Exponents are held as doubles
+ * (integral or -inf) exactly as in the paper; every exponent operation is
+ * exact.  Readings (R#35-R#38):
+ *   R#35  E(x) = getexp = floor(lg|x|) (subnormals exact, E(0) = -inf);
+ *         F(x) = getmant in [1,2) with F(0) = 1, so that 0 = (-inf, 1) as the
+ *         paper states; scalef(x, y) = x 2^y with one rounding,
+ *         scalef(x, -inf) = +-0, scalef(-inf, y) = -inf.
+ *   R#36  the lane of element i (0-based) is i mod s; x is zero-padded to a
+ *         multiple of s (Eq. pad0; zeros leave a partial sum unchanged);
+ *         complex: each iteration takes the real parts, then the imaginary
+ *         parts.
+ *   R#37  lsb of an exponent: cvtpd_epi64(e) & 1, with -inf -> INT64_MIN ->
+ *         0; max(NaN, -inf) = -inf (R#4).
+ *   R#38  the final partial sums are sorted by Eq. (vsort) (the sorted
+ *         sequence is unique: equal keys are equal pairs), then reduced
+ *         pairwise (Eq. redj, SM6.3.2: reduction = 0) or sequentially
+ *         (Eq. reds, SM6.3.3: reduction = 1); s a power of two.
+ * ====================================================================== */
+static double ef_E(double x) { return x == 0.0 ? -INFINITY : (double)ilogb(x); }
+static double ef_F(double x)
+{
+  if (x == 0.0) return 1.0;
+  return scalbn(fabs(x), -ilogb(x));
+}
+static double ef_scalef(double x, double y)
+{
+  if (isinf(y)) return y < 0 ? copysign(0.0, x) : copysign(INFINITY, x);
+  if (isinf(x)) return x;
+  double yy = floor(y);
+  if (yy > 4000.0) yy = 4000.0; /* saturates: the result is +-inf either way */
+  if (yy < -4000.0) yy = -4000.0; /* ... or +-0 */
+  return scalbn(x, (int)yy);
+}
+static double ef_max(double a, double b) { return isnan(a) ? b : (a > b ? a : b); }
+static double ef_lsb(double e)
+{
+  if (isinf(e)) return 0.0; /* cvtpd_epi64(-inf) = INT64_MIN, & 1 = 0 */
+  return (double)(((int64_t)e) & 1);
+}
+/* a <= b by Eq. (vsort) */
+static int ef_le(double ea, double fa, double eb, double fb)
+{
+  return (ea < eb) || (ea == eb && fa <= fb);
+}
+
+/* one update r_{i+1} = fma(|x_i|, |x_i|, r_i) of one lane (Alg SM6.3 lines 5-13) */
+static void ef_update(double *e, double *f, double x)
+{
+  const double eh_lsb = ef_lsb(*e);                      /* line 5-6 */
+  const double ep = *e - eh_lsb;                         /* e' (even or -inf) */
+  const double fp = ef_scalef(*f, eh_lsb);               /* f' */
+  const double ei = ef_E(x), fi = ef_F(x);               /* line 8 */
+  const double eh = ef_scalef(ei, 1.0);                  /* line 9: 2 e_i */
+  const double emax = ef_max(eh, ep);                    /*   e'^(i+1) = e_max */
+  const double eh1 = ef_max(eh - emax, -INFINITY);       /* line 10 */
+  const double epp = ef_max(ep - emax, -INFINITY);
+  const double eh2 = ef_scalef(eh1, -1.0);               /* line 11 */
+  const double fh = ef_scalef(fi, eh2);
+  const double fhp = ef_scalef(fp, epp);
+  const double fpn = fma(fh, fh, fhp);                   /* line 12 */
+  *f = ef_F(fpn);
+  *e = emax + ef_E(fpn);                                 /* line 13 */
+}
+
+/* (a) + (b) for a <= b by Eq. (vsort): Eq. (redj) / (reds), normalised */
+static void ef_add_sorted(double ea, double fa, double eb, double fb, double *e, double *f)
+{
+  const double fpr = fma(ef_scalef(1.0, ef_max(ea - eb, -INFINITY)), fa, fb);
+  *f = ef_F(fpr);
+  *e = eb + ef_E(fpr);
+}
+
+/* ||x||_F of one column (m elements, complex: interleaved) as (e'', f'');
+ * e2/f2 (optional) receive (e, f) of ||x||_F^2 */
+int orc_norm_ef(int cplx, int64_t m, const double *x, int s, int reduction, double *e_out,
+                double *f_out, double *e2, double *f2)
+{
+  if (s < 1 || s > 4096 || (s & (s - 1)) || m < 0) return ORC_EINVAL;
+  double *le = (double *)malloc(sizeof(double) * s), *lf = (double *)malloc(sizeof(double) * s);
+  if (!le || !lf) { free(le); free(lf); return ORC_EINVAL; }
+  for (int l = 0; l < s; ++l) { le[l] = -INFINITY; lf[l] = 1.0; } /* line 2: r_0 = 0 */
+  const int64_t iters = (m + s - 1) / s;
+  for (int64_t it = 0; it < iters; ++it) {
+    for (int part = 0; part < (cplx ? 2 : 1); ++part) {  /* complex: Re, then Im */
+      for (int l = 0; l < s; ++l) {
+        const int64_t i = it * s + l;
+        const double xi = i < m ? (cplx ? x[2 * i + part] : x[i]) : 0.0; /* Eq. pad0 */
+        ef_update(&le[l], &lf[l], xi);
+      }
+    }
+  }
+  /* line 15: sort by Eq. (vsort) (insertion sort: any correct sort gives the same sequence) */
+  for (int a = 1; a < s; ++a) {
+    const double ke = le[a], kf = lf[a];
+    int b = a - 1;
+    while (b >= 0 && !ef_le(le[b], lf[b], ke, kf)) { le[b + 1] = le[b]; lf[b + 1] = lf[b]; --b; }
+    le[b + 1] = ke; lf[b + 1] = kf;
+  }
+  double e, f;
+  if (reduction == 0) { /* lines 16-22: pairwise, Eq. (redj) */
+    for (int w = s; w > 1; w /= 2)
+      for (int i = 0; i < w / 2; ++i)
+        ef_add_sorted(le[2 * i], lf[2 * i], le[2 * i + 1], lf[2 * i + 1], &le[i], &lf[i]);
+  } else { /* Eq. (reds): sequential, swapping out-of-order neighbours */
+    for (int i = 0; i + 1 < s; ++i) {
+      if (!ef_le(le[i], lf[i], le[i + 1], lf[i + 1])) {
+        double t = le[i]; le[i] = le[i + 1]; le[i + 1] = t;
+        t = lf[i]; lf[i] = lf[i + 1]; lf[i + 1] = t;
+      }
+      ef_add_sorted(le[i], lf[i], le[i + 1], lf[i + 1], &le[i + 1], &lf[i + 1]);
+    }
+    le[0] = le[s - 1]; lf[0] = lf[s - 1];
+  }
+  e = le[0]; f = lf[0];
+  free(le); free(lf);
+  if (e2) *e2 = e;
+  if (f2) *f2 = f;
+  /* line 23: the square root, SM6.1 */
+  double ep = e, fp = f;
+  if (!isinf(e) && fmod(e, 2.0) != 0.0) { fp = 2.0 * f; ep = e - 1.0; }
+  *e_out = isinf(ep) ? ep : ep / 2.0;
+  *f_out = sqrt(fp);
+  return ORC_OK;
+}

@@ -15,6 +15,7 @@ __all__ = [
     "hypot_f32", "zeta_f32", "evd2_one_f32", "evd2_batched_f32",
     "upsilon", "gram", "rot", "step", "strategy_pairs", "strategy_is_checkpoint", "Fm",
     "gesvj", "gesvj_batched", "num_threads", "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO",
+    "norm_ef", "norm_ef_cols",
     "OK", "ENOCONV", "EINVAL", "ENONFINITE", "ERANK",
 ]
 
@@ -102,6 +103,9 @@ def lib():
         L.orc_gesvj_batched.argtypes = [ct.c_int, _I64, _I64, _I64, ct.c_void_p, _I64, _I64,
                                         ct.c_void_p, _I64, _I64, ct.c_void_p, ct.c_int32,
                                         ct.c_void_p, ct.c_void_p, ct.POINTER(RSpec)]
+        L.orc_norm_ef.restype = ct.c_int
+        L.orc_norm_ef.argtypes = [ct.c_int, _I64, ct.c_void_p, ct.c_int, ct.c_int, _PD, _PD, _PD,
+                                  _PD]
         L.orc_num_threads.restype = ct.c_int
         L.orc_num_threads.argtypes = []
         _lib = L
@@ -326,3 +330,26 @@ def gesvj_batched(A, R, max_sweeps=30):
     U = np.transpose(G, (0, 2, 1))
     Vm = np.transpose(V, (0, 2, 1))
     return dict(U=U, V=Vm, sigma=sig, sweeps=sw, status=st)
+
+
+def norm_ef(x, s=32, reduction=0):
+    """NEXT-3: ||x||_F by the one-pass (e, f) method of Alg SM6.3
+    with s lanes (R#35-R#38).  x: 1-D float64 or complex128.  reduction 0:
+    pairwise (Eq. redj), 1: sequential (Eq. reds).  Returns (e'', f'', e, f):
+    ||x|| = 2^e'' f'' and ||x||^2 = 2^e f."""
+    x = np.ascontiguousarray(x)
+    cplx = np.iscomplexobj(x)
+    x = x.astype(np.complex128 if cplx else np.float64)
+    e, f, e2, f2 = (ct.c_double() for _ in range(4))
+    st = lib().orc_norm_ef(int(cplx), x.shape[0], _ptr(x), s, reduction, ct.byref(e), ct.byref(f),
+                           ct.byref(e2), ct.byref(f2))
+    if st != 0:
+        raise ValueError("orc_norm_ef: invalid arguments")
+    return e.value, f.value, e2.value, f2.value
+
+
+def norm_ef_cols(A, s=32, reduction=0):
+    """norm_ef of every column of the 2-D array A: arrays (e'', f'')."""
+    n = A.shape[1]
+    out = [norm_ef(A[:, j], s, reduction) for j in range(n)]
+    return np.array([o[0] for o in out]), np.array([o[1] for o in out])
