@@ -591,9 +591,67 @@ class DistC64Workload:
             f"{npairs} of the {self.n // 2} pairs of a step per call (units = fraction of a step)"
 
 
+class NormWorkload:
+    """NEXT-3: the one-pass (e, f) norms (Alg SM6.3, jsvd_norm_ef) of all 8192
+    columns of configs[4]'s complex 32768 x 8192 matrix (4.3 GB, read once)."""
+    graphable = True
+
+    def __init__(self, name, rank, world):
+        import torch
+        import synth
+        self.name, self.unit = name, "columns/s"
+        self.desc = ("NEXT-3 (Alg SM6.3): one-pass (e,f) Frobenius norms of the 8192 columns of "
+                     "BASELINE configs[4]'s complex fp64 32768x8192 matrix, s = 32 lanes")
+        G, _ = synth.svd_cfg5_torch()
+        self.G = G
+        self.m, self.n = G.shape
+        self.ce = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.cf = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        self.units_per_step = self.n
+        self.kernel = "norm_ef_kernel<1>"
+        self.l2_note = "G 4.3 GB >> L2"
+
+    def prepare(self):
+        pass
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        J.norm_ef(self.G, col_e=self.ce, col_f=self.cf, stream=stream)
+
+    def bytes_per_step(self):
+        return self.m * self.n * 16 + self.n * 16
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hG = torch.empty((self.n, self.m), dtype=torch.complex128).pin_memory()
+        hG.copy_(self.G.T)
+        he = torch.empty(self.n, dtype=torch.float64).pin_memory()
+        hf = torch.empty(self.n, dtype=torch.float64).pin_memory()
+        Gt = torch.empty((self.n, self.m), dtype=torch.complex128, device="cuda")
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                Gt.copy_(hG, non_blocking=True)
+                J.norm_ef(Gt.T, col_e=self.ce, col_f=self.cf, stream=stream)
+                he.copy_(self.ce, non_blocking=True)
+                hf.copy_(self.cf, non_blocking=True)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hG.numel() * 16, 2 * self.n * 8
+
+    def cpu_sample(self):
+        import oracle as O
+        k = 16
+        cols = self.G[:, :k].cpu().numpy()
+        return lambda: O.norm_ef_cols(cols), k, f"the first {k} columns per call"
+
+
 WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "evd_c32": EvdWorkload, "step_r64": StepWorkload,
              "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload,
-             "step_c64": StepC64Workload, "dist_c64": DistC64Workload}
+             "step_c64": StepC64Workload, "dist_c64": DistC64Workload, "norm_c64": NormWorkload}
 
 
 def cpu_baseline(wl, target_s=10.0):
@@ -873,9 +931,16 @@ class ReferenceWorkload:
             self.units, self.unit = 1, "sweep-steps/s"
             self.desc = "BASELINE configs[2]: one sweep step of the 4096x1024 real SVD"
             self.what = "one full step (512 pairs) per step"
+        elif name == "norm_c64":
+            rng = np.random.default_rng(5)
+            cols = rng.standard_normal((32768, 4)) + 1j * rng.standard_normal((32768, 4))
+            self.fn = lambda: O.norm_ef_cols(cols)
+            self.units, self.unit = 4, "columns/s"
+            self.desc = NormWorkload.__doc__.strip().split("\n")[0]
+            self.what = "4 complex columns of 32768 rows per step"
         else:
             A = synth.svd_cfg4(16)
-            R = O.RSpec.make(16, 1, [8, 4, 2, 1])  # the batched kernel's R
+            R = O.RSpec.make(8, 1, [4, 2, 1])  # the batched kernel's R (m <= 64)
             self.fn = lambda: O.gesvj_batched(A, R)
             self.units, self.unit = 16, "SVD/s"
             self.desc = "BASELINE configs[3]: complex 64x32 SVDs"
@@ -896,7 +961,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         args.steps = {"evd_c64": 200, "evd_r64": 200, "evd_c32": 200, "step_r64": 300, "gesvj_r64": 2,
-                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100}[args.workload]
+                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100, "norm_c64": 50}[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:

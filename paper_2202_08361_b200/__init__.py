@@ -21,7 +21,7 @@ from ._build import LIB
 
 __all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
            "gesvj_workspace", "gesvj_batched", "launch_count", "evd2_batched_host",
-           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "JsvdError", "R64", "C64",
+           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "norm_ef", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
 R64, C64, R32, C32 = 0, 1, 2, 3
@@ -81,6 +81,8 @@ def lib():
         L.jsvd_gesvj_batched_host.restype = ct.c_int
         L.jsvd_gesvj_batched_host.argtypes = ([ct.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
                                                _vp, _vp, _vp, _i64, _vp, ct.c_size_t, _vp])
+        L.jsvd_norm_ef.restype = ct.c_int
+        L.jsvd_norm_ef.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
         L.jsvd_fp64_peak.restype = ct.c_int
         L.jsvd_fp64_peak.argtypes = [_i32, _i64, _vp, ct.POINTER(_i64), _vp]
         L.jsvd_maxnorm.restype = ct.c_int
@@ -356,6 +358,20 @@ def colnorms(G, col_e=None, col_f=None, stream=None):
     col_f = torch.empty(n, dtype=torch.float64, device=G.device) if col_f is None else col_f
     _check(lib().jsvd_colnorms(C64 if cplx else R64, m, n, _p(G), ld, _p(col_e), _p(col_f),
                                _stream(stream)), "jsvd_colnorms")
+    return col_e, col_f
+
+
+def norm_ef(G, col_e=None, col_f=None, col_e2=None, col_f2=None, stream=None):
+    """NEXT-3: ||g_j|| of every column of column-major G by the one-pass (e, f)
+    method of Alg SM6.3 (s = 32 lanes, jsvd_norm_ef).  Returns (col_e, col_f)
+    with ||g_j|| = 2^col_e col_f; pass col_e2/col_f2 tensors to also get the
+    (e, f) of ||g_j||^2."""
+    cplx, ld = _mat(G, "G")
+    m, n = G.shape
+    col_e = torch.empty(n, dtype=torch.float64, device=G.device) if col_e is None else col_e
+    col_f = torch.empty(n, dtype=torch.float64, device=G.device) if col_f is None else col_f
+    _check(lib().jsvd_norm_ef(C64 if cplx else R64, m, n, _p(G), ld, _p(col_e), _p(col_f),
+                              _p(col_e2), _p(col_f2), _stream(stream)), "jsvd_norm_ef")
     return col_e, col_f
 
 
