@@ -44,8 +44,8 @@ __device__ __forceinline__ void ef_norm(double v, int& de, double& f) {
                                                   0x3ff0000000000000ull));
 }
 
-// r <- fma(|x|, |x|, r) (Alg SM6.3 lines 5-13) for one lane
-__device__ __forceinline__ void ef_update(int& e, double& f, double x) {
+// r <- fma(|x|, |x|, r) (Alg SM6.3 lines 5-13) for one lane: every case
+__device__ __forceinline__ void ef_update_general(int& e, double& f, double x) {
   const bool einf = e == kNegInf;
   const int lsb = einf ? 0 : (e & 1);           // cvtpd_epi64(e) & 1, -inf -> 0 (R#37)
   const int ep = einf ? kNegInf : e - lsb;      // e' (even or -inf)
@@ -69,6 +69,44 @@ __device__ __forceinline__ void ef_update(int& e, double& f, double x) {
     ef_norm(fpn, de, f);
     e = emax + de;
   }
+}
+
+// The same update with the common case on the integer pipe: r != 0 and x
+// normal, and both scalings 2^{e-hat''}, 2^{e''} >= 2^-1022.  Then f' = f or 2f
+// is an exponent-field add, E(x) and F(x) are bit fields, and the two scalef
+// are exact multiplies by normal powers of two (f_i in [1,2), f' in [1,4)):
+// only the fma rounds, exactly as in the general form.  Lanes outside that
+// case take ef_update_general in a warp-uniform branch (the first element of
+// every lane, zeros, subnormals, and sums 2^2044 apart).
+__device__ __forceinline__ void ef_update(int& e, double& f, double x) {
+  const uint32_t hx = hi32(x) & 0x7fffffffu;
+  const int lsb = e & 1;
+  const int ep = e - lsb;
+  const double fp = mkd(hi32(f) + (static_cast<uint32_t>(lsb) << 20), lo32(f));
+  const int eh = 2 * (static_cast<int>(hx >> 20) - 1023);
+  const double fi = mkd((hx & 0x000fffffu) | 0x3ff00000u, lo32(x));
+  const int emax = max(eh, ep);
+  const int h2 = (eh - emax) >> 1;  // even and <= 0: exact halving
+  const int d2 = ep - emax;
+  const bool fast = (e != kNegInf) & (hx >= 0x00100000u) & (h2 >= -1022) & (d2 >= -1022);
+  const double fh = fi * pow2i(max(h2, -1022));
+  const double fhp = fp * pow2i(max(d2, -1022));
+  const double fpn = fma(fh, fh, fhp);
+  int de;
+  double fn;
+  ef_norm(fpn, de, fn);
+  int en = emax + de;
+  if (__any_sync(0xffffffffu, !fast)) {
+    int eg = e;
+    double fg = f;
+    ef_update_general(eg, fg, x);
+    if (!fast) {
+      en = eg;
+      fn = fg;
+    }
+  }
+  e = en;
+  f = fn;
 }
 
 // a + b for a <= b by Eq. (vsort): Eq. (redj), normalised
