@@ -863,3 +863,22 @@ int orc_norm_ef(int cplx, int64_t m, const double *x, int s, int reduction, doub
   *f_out = sqrt(fp);
   return ORC_OK;
 }
+
+/* ======================================================================
+ * NEXT-4: the real Gram-Schmidt orthogonalization dgsscl of Alg SM8.1 /
+ * Eq. (DGS), one pair, statement by statement:
+ *   -psi = -(a21' (f_q / f_p))                       (line 1; R#39)
+ *   x = scalef(g_p, -e_p); y = scalef(g_q, -e_q)      (line 4)
+ *   g_q' = scalef(fma(-psi, x, y), e_q)               (line 5)
+ * g_p is unchanged.  (e_j, f_j) = ||g_j|| are inputs (> 0, finite).
+ * ====================================================================== */
+void orc_dgsscl(int64_t m, const double *gp, double *gq, double ep, double fp, double eq,
+                double fq, double a21)
+{
+  const double mpsi = -(a21 * (fq / fp));
+  for (int64_t i = 0; i < m; ++i) {
+    const double x = scalbn(gp[i], (int)-ep);
+    const double y = scalbn(gq[i], (int)-eq);
+    gq[i] = scalbn(fma(mpsi, x, y), (int)eq);
+  }
+}

@@ -15,7 +15,7 @@ __all__ = [
     "hypot_f32", "zeta_f32", "evd2_one_f32", "evd2_batched_f32",
     "upsilon", "gram", "rot", "step", "strategy_pairs", "strategy_is_checkpoint", "Fm",
     "gesvj", "gesvj_batched", "num_threads", "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO",
-    "norm_ef", "norm_ef_cols",
+    "norm_ef", "norm_ef_cols", "dgsscl",
     "OK", "ENOCONV", "EINVAL", "ENONFINITE", "ERANK",
 ]
 
@@ -106,6 +106,8 @@ def lib():
         L.orc_norm_ef.restype = ct.c_int
         L.orc_norm_ef.argtypes = [ct.c_int, _I64, ct.c_void_p, ct.c_int, ct.c_int, _PD, _PD, _PD,
                                   _PD]
+        L.orc_dgsscl.restype = None
+        L.orc_dgsscl.argtypes = [_I64, ct.c_void_p, ct.c_void_p, _D, _D, _D, _D, _D]
         L.orc_num_threads.restype = ct.c_int
         L.orc_num_threads.argtypes = []
         _lib = L
@@ -353,3 +355,12 @@ def norm_ef_cols(A, s=32, reduction=0):
     n = A.shape[1]
     out = [norm_ef(A[:, j], s, reduction) for j in range(n)]
     return np.array([o[0] for o in out]), np.array([o[1] for o in out])
+
+
+def dgsscl(gp, gq, ep, fp, eq, fq, a21):
+    """NEXT-4: real Gram-Schmidt orthogonalization of g_q against g_p, Alg SM8.1 /
+    Eq. (DGS) (P:1369-1396, P:3812-3832; R#39).  Returns the new g_q."""
+    gp = np.ascontiguousarray(gp, dtype=np.float64)
+    out = np.array(gq, dtype=np.float64, copy=True)
+    lib().orc_dgsscl(gp.shape[0], _ptr(gp), _ptr(out), ep, fp, eq, fq, a21)
+    return out
