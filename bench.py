@@ -649,9 +649,74 @@ class NormWorkload:
         return lambda: O.norm_ef_cols(cols), k, f"the first {k} columns per call"
 
 
+class GsWorkload:
+    """NEXT-4: the real Gram-Schmidt orthogonalization (Alg SM8.1, jsvd_dgsscl)
+    of all 4096 disjoint column pairs of a real 32768 x 8192 matrix (2.1 GB)."""
+    graphable = True
+
+    def __init__(self, name, rank, world):
+        import torch
+        import paper_2202_08361_b200 as J
+        self.name, self.unit = name, "pairs/s"
+        self.desc = ("NEXT-4 (Alg SM8.1): Gram-Schmidt of g_q against g_p for the 4096 pairs of a real "
+                     "fp64 32768x8192 matrix (configs[4]'s shape), one round-robin step's pairs")
+        self.m, self.n = 32768, 8192
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(5 + rank)
+        self.G = torch.randn((self.n, self.m), dtype=torch.float64, device="cuda",
+                             generator=gen).T
+        self.pairs = J.strategy_pairs(self.n, self.n, 0).contiguous()
+        self.ce, self.cf = J.colnorms(self.G)
+        self.a21 = torch.rand(self.n // 2, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+        self.units_per_step = self.n // 2
+        self.kernel = "dgsscl_kernel"
+        self.l2_note = "G 2.1 GB >> L2"
+
+    def prepare(self):
+        pass
+
+    def step(self, stream):
+        import paper_2202_08361_b200 as J
+        J.dgsscl(self.G, self.pairs, self.ce, self.cf, self.a21, stream=stream)
+
+    def bytes_per_step(self):
+        return (self.n // 2) * 3 * self.m * 8
+
+    def e2e(self, stream, steps):
+        import torch
+        import paper_2202_08361_b200 as J
+        hG = torch.empty((self.n, self.m), dtype=torch.float64).pin_memory()
+        hG.copy_(self.G.T)
+        Gt = torch.empty((self.n, self.m), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            Gt.copy_(hG, non_blocking=True)
+            J.dgsscl(Gt.T, self.pairs, self.ce, self.cf, self.a21, stream=stream)
+            hG.copy_(Gt, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), hG.numel() * 8, hG.numel() * 8
+
+    def cpu_sample(self):
+        import oracle as O
+        k = 64
+        G = self.G[:, :2 * k].cpu().numpy()
+        ce, cf = self.ce.cpu().numpy(), self.cf.cpu().numpy()
+        a = self.a21.cpu().numpy()
+
+        def run():
+            for l in range(k):
+                O.dgsscl(G[:, 2 * l], G[:, 2 * l + 1], ce[2 * l], cf[2 * l], ce[2 * l + 1],
+                         cf[2 * l + 1], a[l])
+        return run, k, f"{k} pairs of 32768 rows per call"
+
+
 WORKLOADS = {"evd_c64": EvdWorkload, "evd_r64": EvdWorkload, "evd_c32": EvdWorkload, "step_r64": StepWorkload,
              "gesvj_r64": GesvjWorkload, "batched_c64": BatchedWorkload,
-             "step_c64": StepC64Workload, "dist_c64": DistC64Workload, "norm_c64": NormWorkload}
+             "step_c64": StepC64Workload, "dist_c64": DistC64Workload, "norm_c64": NormWorkload,
+             "gs_r64": GsWorkload}
 
 
 def cpu_baseline(wl, target_s=10.0):
@@ -961,7 +1026,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         args.steps = {"evd_c64": 200, "evd_r64": 200, "evd_c32": 200, "step_r64": 300, "gesvj_r64": 2,
-                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100, "norm_c64": 50}[args.workload]
+                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100, "norm_c64": 50,
+                      "gs_r64": 50}[args.workload]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -870,11 +870,13 @@ int orc_norm_ef(int cplx, int64_t m, const double *x, int s, int reduction, doub
  *   -psi = -(a21' (f_q / f_p))                       (line 1; R#39)
  *   x = scalef(g_p, -e_p); y = scalef(g_q, -e_q)      (line 4)
  *   g_q' = scalef(fma(-psi, x, y), e_q)               (line 5)
- * g_p is unchanged.  (e_j, f_j) = ||g_j|| are inputs (> 0, finite).
+ * g_p is unchanged.  (e_j, f_j) = ||g_j|| are inputs (> 0, finite); a pair
+ * with a zero column (e = -inf, R#19) is left as it is.
  * ====================================================================== */
 void orc_dgsscl(int64_t m, const double *gp, double *gq, double ep, double fp, double eq,
                 double fq, double a21)
 {
+  if (isinf(ep) || isinf(eq)) return; /* a zero column (R#19): nothing to orthogonalise */
   const double mpsi = -(a21 * (fq / fp));
   for (int64_t i = 0; i < m; ++i) {
     const double x = scalbn(gp[i], (int)-ep);

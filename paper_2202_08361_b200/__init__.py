@@ -21,7 +21,7 @@ from ._build import LIB
 
 __all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
            "gesvj_workspace", "gesvj_batched", "launch_count", "evd2_batched_host",
-           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "norm_ef", "JsvdError", "R64", "C64",
+           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "norm_ef", "dgsscl", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
 R64, C64, R32, C32 = 0, 1, 2, 3
@@ -83,6 +83,8 @@ def lib():
                                                _vp, _vp, _vp, _i64, _vp, ct.c_size_t, _vp])
         L.jsvd_norm_ef.restype = ct.c_int
         L.jsvd_norm_ef.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+        L.jsvd_dgsscl.restype = ct.c_int
+        L.jsvd_dgsscl.argtypes = [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
         L.jsvd_fp64_peak.restype = ct.c_int
         L.jsvd_fp64_peak.argtypes = [_i32, _i64, _vp, ct.POINTER(_i64), _vp]
         L.jsvd_maxnorm.restype = ct.c_int
@@ -373,6 +375,23 @@ def norm_ef(G, col_e=None, col_f=None, col_e2=None, col_f2=None, stream=None):
     _check(lib().jsvd_norm_ef(C64 if cplx else R64, m, n, _p(G), ld, _p(col_e), _p(col_f),
                               _p(col_e2), _p(col_f2), _stream(stream)), "jsvd_norm_ef")
     return col_e, col_f
+
+
+def dgsscl(G, pairs, col_e, col_f, a21, stream=None):
+    """NEXT-4: real Gram-Schmidt orthogonalization (Alg SM8.1 / Eq. DGS,
+    jsvd_dgsscl) of g_q against g_p for each pair, in place on column-major
+    float64 G.  pairs: int32 (npairs, 2); col_e/col_f: the columns' norms
+    (e, f); a21: float64 (npairs,) the pairs' scaled dots a21'."""
+    cplx, ld = _mat(G, "G")
+    if cplx:
+        raise ValueError("dgsscl is real only (the paper's complex variant is not given)")
+    m, n = G.shape
+    pairs = pairs.reshape(-1)
+    if pairs.dtype != torch.int32 or not pairs.is_contiguous():
+        raise ValueError("pairs must be contiguous int32")
+    _check(lib().jsvd_dgsscl(m, n, _p(G), ld, _p(pairs), pairs.numel() // 2, _p(col_e), _p(col_f),
+                             _p(_f64(a21, "a21")), _stream(stream)), "jsvd_dgsscl")
+    return G
 
 
 def normalize(G, col_e, col_f, stream=None):
