@@ -145,10 +145,11 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
                                cudaStream_t st) {
   const int threads = 256;
   if (!CPLX) {
-    // real (configs[0]): one matrix per thread at <= 40 registers, 6 CTAs per
-    // SM -- the short (~15 us) launch is latency- and tail-bound, and 48 warps
-    // per SM measured better than the 2-per-thread vector kernel (59% -> 63%
-    // of the HBM peak); 8-byte-aligned pointers suffice
+    // real (configs[0]): one matrix per thread at 32 registers, 8 CTAs per
+    // SM (64 warps, the maximum) -- the short (~15 us) launch is latency- and
+    // tail-bound: 59% of the HBM peak with the 2-per-thread vector kernel, 63%
+    // at 6 CTAs/SM, 67% at 8 (despite 96 bytes of L1-resident spills);
+    // 8-byte-aligned pointers suffice
     const int64_t blocks = (r + threads - 1) / threads;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(blocks));
@@ -159,7 +160,7 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 6>, r, a11, a22, re, im, l1, l2,
+    cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8>, r, a11, a22, re, im, l1, l2,
                        c, sr, si, zeta, perm);
     note_launch();
     return cudaGetLastError();
