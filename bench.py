@@ -766,7 +766,7 @@ def run_jsvd(args):
     # timed as one replay: the device time of the K launches without the
     # Python/ctypes enqueue cost between them
     graph = None
-    if getattr(wl, "graphable", False) and world == 1 and not args.no_graph:
+    if getattr(wl, "graphable", False) and not args.no_graph:  # per rank, no collective inside
         graph = torch.cuda.CUDAGraph()
         nc0 = J.launch_count()
         with torch.cuda.graph(graph):
