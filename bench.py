@@ -112,6 +112,19 @@ def _ncores():
 
 
 # --------------------------------------------------------------- workloads
+# workload descriptions shared by both arms (config.workload of the JSON line)
+DESC = {
+    "evd_c64": "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 per GPU, seed 7",
+    "evd_r64": "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 per GPU, seed 42",
+    "evd_c32": ("single-precision analogue of BASELINE configs[1] (NEXT-1, P:709-717): "
+                "batched complex Hermitian 2x2 EVD, fp32, r=2^26 per GPU, seed 7"),
+    "batched_c64": ("BASELINE configs[3]: batch of 65536 complex fp64 64x32 matrices, "
+                    "re,im ~ N(0,1), full Jacobi SVD (U, Sigma, V) of each, seed 4"),
+    "norm_c64": ("NEXT-3 (Alg SM6.3): one-pass (e,f) Frobenius norms of the 8192 columns of "
+                 "BASELINE configs[4]'s complex fp64 32768x8192 matrix, s = 32 lanes"),
+}
+
+
 class EvdWorkload:
     """configs[0] / configs[1]: batched 2x2 EVD (jsvd_evd2_batched)."""
     graphable = True
@@ -125,14 +138,13 @@ class EvdWorkload:
         self.r = (1 << 26) if self.cplx else (1 << 20)
         self.unit = "EVD/s"
         if self.f32:
-            self.desc = ("single-precision analogue of BASELINE configs[1] (NEXT-1, P:709-717): "
-                         "batched complex Hermitian 2x2 EVD, fp32, r=2^26 per GPU, seed 7")
+            self.desc = DESC["evd_c32"]
             self.host = synth.evd_cfg2_f32(self.r, off=rank * self.r)
         elif self.cplx:
-            self.desc = "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 per GPU, seed 7"
+            self.desc = DESC["evd_c64"]
             self.host = synth.evd_cfg2(self.r, off=rank * self.r)
         else:
-            self.desc = "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 per GPU, seed 42"
+            self.desc = DESC["evd_r64"]
             self.host = synth.evd_cfg1(self.r, off=rank * self.r)
         w = 4 if self.f32 else 8
         self.unit_bytes = (9 * w + 4 + 1 / 8) if self.cplx else (7 * w + 4 + 1 / 8)
@@ -301,8 +313,7 @@ class BatchedWorkload:
         import synth
         self.name, self.unit = name, "SVD/s"
         self.b, self.m, self.n = 65536, 64, 32
-        self.desc = ("BASELINE configs[3]: batch of 65536 complex fp64 64x32 matrices, "
-                     "re,im ~ N(0,1), full Jacobi SVD (U, Sigma, V) of each, seed 4")
+        self.desc = DESC["batched_c64"]
         self.host = synth.svd_cfg4(self.b, off=rank * self.b)
         self.A0 = torch.from_numpy(np.ascontiguousarray(np.transpose(self.host, (0, 2, 1)))).cuda()
         self.A = torch.empty_like(self.A0)
@@ -600,8 +611,7 @@ class NormWorkload:
         import torch
         import synth
         self.name, self.unit = name, "columns/s"
-        self.desc = ("NEXT-3 (Alg SM6.3): one-pass (e,f) Frobenius norms of the 8192 columns of "
-                     "BASELINE configs[4]'s complex fp64 32768x8192 matrix, s = 32 lanes")
+        self.desc = DESC["norm_c64"]
         G, _ = synth.svd_cfg5_torch()
         self.G = G
         self.m, self.n = G.shape
@@ -983,7 +993,7 @@ class ReferenceWorkload:
                 a = synth.evd_cfg2(n) if name == "evd_c64" else synth.evd_cfg1(n)
                 self.fn = lambda: O.evd2_batched(*a)
             self.units, self.unit = n, "EVD/s"
-            self.desc = EvdWorkload.__doc__.strip().split("\n")[0] + f" ({name})"
+            self.desc = DESC[name]
             self.what = f"{n} matrices of the batch per step"
         elif name in ("step_r64", "gesvj_r64"):
             A, _ = synth.svd_cfg3()
@@ -1002,14 +1012,14 @@ class ReferenceWorkload:
             cols = rng.standard_normal((32768, 4)) + 1j * rng.standard_normal((32768, 4))
             self.fn = lambda: O.norm_ef_cols(cols)
             self.units, self.unit = 4, "columns/s"
-            self.desc = NormWorkload.__doc__.strip().split("\n")[0]
+            self.desc = DESC["norm_c64"]
             self.what = "4 complex columns of 32768 rows per step"
         else:
             A = synth.svd_cfg4(16)
             R = O.RSpec.make(8, 1, [4, 2, 1])  # the batched kernel's R (m <= 64)
             self.fn = lambda: O.gesvj_batched(A, R)
             self.units, self.unit = 16, "SVD/s"
-            self.desc = "BASELINE configs[3]: complex 64x32 SVDs"
+            self.desc = DESC["batched_c64"]
             self.what = "16 matrices of the batch per step"
 
 
