@@ -43,6 +43,34 @@ def test_library_loads_and_answers_host_only_calls():
     assert L.jsvd_evd2_batched(0, 0, *([None] * 11), 0, None) == 0
 
 
+def test_host_pipeline_argument_checks_without_gpu():
+    # jsvd_evd2_batched_host / jsvd_gesvj_batched_host validate before any CUDA call
+    import ctypes as ct
+    import numpy as np
+    import paper_2202_08361_b200 as J
+    L = J.lib()
+    b = ct.c_size_t()
+    assert L.jsvd_evd2_host_workspace(1, 48, ct.byref(b)) == -1      # chunk not a multiple of 32
+    assert L.jsvd_evd2_host_workspace(1, 1 << 20, ct.byref(b)) == 0
+    per_slot_c64 = 9 * 8 * (1 << 20) + 4 * (1 << 20) + 4 * ((1 << 20) // 32)
+    assert b.value == 3 * per_slot_c64
+    assert L.jsvd_evd2_host_workspace(0, 1 << 20, ct.byref(b)) == 0
+    assert b.value == 3 * (7 * 8 * (1 << 20) + 4 * (1 << 20) + 4 * ((1 << 20) // 32))
+    x = np.zeros(64)
+    p = ct.c_void_p(x.ctypes.data)
+    args = [p] * 4 + [p] * 5 + [None, None]
+    # workspace smaller than the query -> ENOMEM, nothing launched
+    assert L.jsvd_evd2_batched_host(1, 64, *args, 0, 32, p, 16, None) == -6
+    # r == 0 is a no-op; complex without a21_im -> EINVAL
+    assert L.jsvd_evd2_batched_host(1, 0, *args, 0, 32, None, 0, None) == 0
+    assert L.jsvd_evd2_batched_host(1, 64, *([p] * 3 + [None] + [p] * 5 + [None, None]), 0, 32,
+                                    p, 1 << 30, None) == -1
+    assert L.jsvd_gesvj_batched_host_workspace(2, 64, 32, 8, ct.byref(b)) == -1  # R32: SVD is fp64
+    assert L.jsvd_gesvj_batched_host_workspace(1, 64, 32, 8, ct.byref(b)) == 0 and b.value > 0
+    assert L.jsvd_gesvj_batched_host(1, 4, 64, 32, p, p, p, p, 30, None, None, None, 2, p, 16,
+                                     None) == -6
+
+
 def test_sm100a_code_in_library():
     from paper_2202_08361_b200 import _build
     lib = _build.build()
