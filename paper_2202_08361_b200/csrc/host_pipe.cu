@@ -7,7 +7,6 @@
 // internal streams and events are created once per device.  Results are the
 // device entry points' (the same kernels on the same data), bit for bit.
 #include <mutex>
-#include <vector>
 
 #include "jsvd_host.h"
 
@@ -22,30 +21,30 @@ struct PipeStreams {
   cudaEvent_t e[kSlots + 1] = {};
 };
 
+constexpr int kMaxDevices = 64;
 std::mutex g_pipe_mu;
-std::vector<PipeStreams> g_pipes;
+PipeStreams g_pipes[kMaxDevices];  // per device, created once, never moved
 
-// the internal streams / events of the current device (created once)
+// the internal streams / events of the current device (created once).  Calls
+// from several host threads on one device share them: every cross-stream edge
+// is captured when it is enqueued, so interleaved calls can only over-order.
 cudaError_t pipe_streams(PipeStreams** out) {
   int dev = 0;
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> g(g_pipe_mu);
-  for (auto& p : g_pipes)
-    if (p.dev == dev) {
-      *out = &p;
-      return cudaSuccess;
+  PipeStreams& p = g_pipes[dev];
+  if (p.dev != dev) {
+    for (int k = 0; k < kSlots; ++k) {
+      if ((err = cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking)) != cudaSuccess) return err;
     }
-  PipeStreams p;
-  p.dev = dev;
-  for (int k = 0; k < kSlots; ++k) {
-    if ((err = cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking)) != cudaSuccess) return err;
+    for (int k = 0; k <= kSlots; ++k) {
+      if ((err = cudaEventCreateWithFlags(&p.e[k], cudaEventDisableTiming)) != cudaSuccess) return err;
+    }
+    p.dev = dev;
   }
-  for (int k = 0; k <= kSlots; ++k) {
-    if ((err = cudaEventCreateWithFlags(&p.e[k], cudaEventDisableTiming)) != cudaSuccess) return err;
-  }
-  g_pipes.push_back(p);
-  *out = &g_pipes.back();
+  *out = &p;
   return cudaSuccess;
 }
 
