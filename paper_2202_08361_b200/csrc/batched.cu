@@ -23,6 +23,7 @@
 //      M-tilde tracked by its high word (only floor(lg M-tilde) enters Eq. skr)
 // The Eq. (skr) rescale check runs at every step (flat round-robin, R#21).
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "jsvd_host.h"
@@ -107,7 +108,7 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
 }
 
 // FULL: m == W NR (configs[3]: 64 = 8 x 8), so no row needs a bounds check
-template <bool CPLX, int NR, bool FULL, int W>
+template <bool CPLX, int NR, bool FULL, int W, int VH = 0>
 __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
@@ -123,7 +124,10 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   PairSlot* slots2 = reinterpret_cast<PairSlot*>(sG + m * n);  // [2][n/2]: steps alternate
   double* ce = reinterpret_cast<double*>(slots2 + n);
   double* cf = ce + n;
-  uint8_t* sPairs = reinterpret_cast<uint8_t*>(cf + n);  // (n-1) x n/2 pivot pairs (n <= 64)
+  // rows 0..VH-1 of the working V in shared memory (column-major, VH x n): the
+  // fast half of every V rotation; rows VH.. live in A's storage
+  E* sVh = reinterpret_cast<E*>(cf + n);
+  uint8_t* sPairs = reinterpret_cast<uint8_t*>(sVh + VH * n);  // (n-1) x n/2 pivot pairs (n <= 64)
   __shared__ unsigned long long sM0;
   __shared__ uint32_t sMt;  // high word of M-tilde (its floor(lg) is all Eq. skr uses)
   __shared__ int sT;
@@ -183,8 +187,11 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   // cta_max_u64)
   for (int k = threadIdx.x; k < ni * ni; k += kBT) {
     const int j = k / ni, i = k - j * ni;
-    if constexpr (CPLX) Ag[static_cast<int64_t>(j) * lda + i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    else Ag[static_cast<int64_t>(j) * lda + i] = i == j ? 1.0 : 0.0;
+    E v;
+    if constexpr (CPLX) v = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    else v = i == j ? 1.0 : 0.0;
+    if (i < VH) sVh[j * VH + i] = v;
+    else Ag[static_cast<int64_t>(j) * lda + i] = v;
   }
   __syncthreads();
 
@@ -200,8 +207,18 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       E* vp = Ag + static_cast<int64_t>(p) * lda;
       E* vq = Ag + static_cast<int64_t>(q) * lda;
       // one row at a time: prefetching rows costs registers, and at the
-      // 96-register cap of 5 CTAs per SM any spill costs more than it hides
-      for (int i = lane0; i < ni; i += lanes) {
+      // 96-register cap of 5 CTAs per SM any spill costs more than it hides;
+      // the shared-memory rows first (short latency), then the global ones
+      int i = lane0;
+      for (; i < VH && i < ni; i += lanes) {
+        E* sp = sVh + p * VH;
+        E* sq = sVh + q * VH;
+        E a = sp[i], bq = sq[i];
+        rot_elem(a, bq, sl.c, sl.C, sl.S);
+        sp[i] = a;
+        sq[i] = bq;
+      }
+      for (; i < ni; i += lanes) {
         E a = vp[i], bq = vq[i];
         rot_elem(a, bq, sl.c, sl.C, sl.S);
         vp[i] = a;
@@ -410,7 +427,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     // V's output column r0 from the working V in A's storage
     E* vcol = Vb + static_cast<int64_t>(r0) * ldv;
     const E* vw = Ag + static_cast<int64_t>(j) * lda;
-    for (int i = lane; i < ni; i += 32) vcol[i] = vw[i];
+    for (int i = lane; i < ni; i += 32) vcol[i] = i < VH ? sVh[j * VH + i] : vw[i];
     if (lane == 0) {
       const double e = ce[j], f = cf[j];
       const bool fin = !isinf(e);
@@ -446,9 +463,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
 // lanes per pair of the kernel jsvd_gesvj_batched launches for m (R.W)
 static int batched_w(int64_t m) { return m <= 64 ? 8 : 16; }
 
-static size_t batched_smem(bool cplx, int64_t m, int64_t n) {
+static size_t batched_smem(bool cplx, int64_t m, int64_t n, int vh = 0) {
   const size_t w = cplx ? 16 : 8;
-  return w * (m * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n +
+  return w * (m * n) + sizeof(PairSlot) * n + 2 * sizeof(double) * n + w * vh * n +
          2 * (n - 1) * (n / 2);
 }
 
@@ -490,9 +507,31 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                                               transforms, Fm, Kr, tol);
   };
   // W = batched_w(m) lanes per pair; NR = rows per lane
+  // 16 rows of V in shared memory when 5 CTAs per SM still fit (64 x 32 complex)
+  const size_t smem16 = batched_smem(cplx, m, n, 16);
+  auto go16 = [&](auto kern, int threads) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem16));
+    kern<<<static_cast<unsigned>(batch), threads, smem16, st>>>(m, n, A, lda, strideA, V, ldv,
+                                                                strideV, sigma, max_sweeps,
+                                                                sweeps_done, status, transforms, Fm,
+                                                                Kr, tol);
+  };
+  static const int vh_env = [] {
+    const char* v = getenv("JSVD_BATCHED_VH");
+    return v ? atoi(v) : 1;
+  }();
+  bool vh16 = false;
+  if (vh_env && n <= 32) {
+    int dev = 0, per_sm = 0, reserved = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    vh16 = 5 * (smem16 + 320 + static_cast<size_t>(reserved)) <= static_cast<size_t>(per_sm);
+  }
   auto pick = [&](auto cplx_t) {
     constexpr bool C = decltype(cplx_t)::value;
     if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    else if (m == 64 && vh16) go16(batched_svd_kernel<C, 8, true, 8, 16>, 128);
     else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
     else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);
     else if (m < 64) go(batched_svd_kernel<C, 8, false, 8>, 128);
