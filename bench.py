@@ -742,8 +742,19 @@ def cpu_baseline(wl, target_s=10.0):
         if time.perf_counter() - t0 > target_s or reps >= 100000:
             break
     dt = time.perf_counter() - t0
-    return {"value": units * reps / dt, "unit": wl.unit, "cores": O.num_threads(),
-            "kind": "oracle", "sample": f"{what} x {reps} calls ({dt:.1f} s)"}
+    out = {"value": units * reps / dt, "unit": wl.unit, "cores": O.num_threads(),
+           "kind": "oracle", "sample": f"{what} x {reps} calls ({dt:.1f} s)"}
+    if isinstance(wl, EvdWorkload):  # also one core for configs 1-2
+        nt = O.num_threads()
+        O.set_num_threads(1)
+        t0, reps1 = time.perf_counter(), 0
+        while time.perf_counter() - t0 < target_s / 4 and reps1 < 100000:
+            fn()
+            reps1 += 1
+        dt1 = time.perf_counter() - t0
+        O.set_num_threads(nt)
+        out["value_1core"] = units * reps1 / dt1
+    return out
 
 
 def run_jsvd(args):
@@ -847,7 +858,9 @@ def run_jsvd(args):
     achieved = bytes_step / (ms_per_step / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.workload),
-                "peak_source": peak_src, "kernel": wl.kernel}
+                "peak_source": peak_src, "kernel": wl.kernel,
+                # SURVEY 8(d).1 reports both: the measured copy peak and the nominal ~8 TB/s
+                "nominal_peak": 8000.0, "nominal_frac": achieved / 8000.0}
     if isinstance(wl, EvdWorkload) and wl.nsets > 1:  # the short configs[0] launch
         extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
     if isinstance(wl, GesvjWorkload):

@@ -884,3 +884,14 @@ void orc_dgsscl(int64_t m, const double *gp, double *gq, double ep, double fp, d
     gq[i] = scalbn(fma(mpsi, x, y), (int)eq);
   }
 }
+
+/* the number of OpenMP threads the batched oracle entry points use (timing
+ * only: results do not depend on it) */
+void orc_set_num_threads(int t)
+{
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}

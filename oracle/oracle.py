@@ -14,7 +14,7 @@ __all__ = [
     "RSpec", "lib", "hypot", "zeta", "evd2_one", "evd2_batched", "colnorm", "dot", "cvg",
     "hypot_f32", "zeta_f32", "evd2_one_f32", "evd2_batched_f32",
     "upsilon", "gram", "rot", "step", "strategy_pairs", "strategy_is_checkpoint", "Fm",
-    "gesvj", "gesvj_batched", "num_threads", "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO",
+    "gesvj", "gesvj_batched", "num_threads", "set_num_threads", "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO",
     "norm_ef", "norm_ef_cols", "dgsscl",
     "OK", "ENOCONV", "EINVAL", "ENONFINITE", "ERANK",
 ]
@@ -108,6 +108,8 @@ def lib():
                                   _PD]
         L.orc_dgsscl.restype = None
         L.orc_dgsscl.argtypes = [_I64, ct.c_void_p, ct.c_void_p, _D, _D, _D, _D, _D]
+        L.orc_set_num_threads.restype = None
+        L.orc_set_num_threads.argtypes = [ct.c_int]
         L.orc_num_threads.restype = ct.c_int
         L.orc_num_threads.argtypes = []
         _lib = L
@@ -125,6 +127,11 @@ def _f64(a):
 
 def num_threads():
     return lib().orc_num_threads()
+
+
+def set_num_threads(t):
+    """OpenMP threads of the batched entry points (timing only)."""
+    lib().orc_set_num_threads(int(t))
 
 
 def hypot(x, y):
