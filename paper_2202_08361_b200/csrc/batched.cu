@@ -516,10 +516,10 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                                                 sweeps_done, status, transforms, Fm,
                                                                 Kr, tol);
   };
-  static const int vh_env = [] {
-    const char* v = getenv("JSVD_BATCHED_VH");
-    return v ? atoi(v) : 1;
-  }();
+  // JSVD_BATCHED_VH=0 keeps all of V in A's storage (same results, bit for
+  // bit: only where V lives changes; the GPU tests compare both)
+  const char* vh_s = getenv("JSVD_BATCHED_VH");
+  const int vh_env = vh_s ? atoi(vh_s) : 1;
   bool vh16 = false;
   if (vh_env && n <= 32) {
     int dev = 0, per_sm = 0, reserved = 0;

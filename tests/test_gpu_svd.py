@@ -233,3 +233,27 @@ def test_gesvj_batched_mixed_status_and_caps(J, cplx, max_sweeps):
     V = out["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
     assert bits_equal(U[ok], ref["U"][ok]) and bits_equal(V[ok], ref["V"][ok])
     assert bits_equal(out["sigma"].cpu().numpy()[ok], ref["sigma"][ok])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_batched_v_placement_is_invisible(J, monkeypatch, cplx):
+    # half of the working V in shared memory (default) or all of it in A's
+    # storage (JSVD_BATCHED_VH=0): the same arithmetic, so the same bits
+    rng = np.random.default_rng(31 + cplx)
+    b, m, n = 40, 64, 32
+    A = rng.standard_normal((b, m, n)) * 2.0 ** rng.integers(-40, 40, (b, 1, n))
+    if cplx:
+        A = A + 1j * rng.standard_normal((b, m, n))
+    outs = []
+    for vh in ("1", "0"):
+        monkeypatch.setenv("JSVD_BATCHED_VH", vh)
+        g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+        o = J.gesvj_batched(g, max_sweeps=30)
+        torch.cuda.synchronize()
+        outs.append({k: o[k].transpose(1, 2).contiguous().cpu() if k in ("U", "V") else o[k].cpu()
+                     for k in ("U", "V", "sigma", "sweeps", "status")})
+    for k in outs[0]:
+        a, c = outs[0][k], outs[1][k]
+        if a.is_complex():
+            a, c = torch.view_as_real(a), torch.view_as_real(c)
+        assert torch.equal(a, c), k
