@@ -1062,6 +1062,37 @@ class ReferenceWorkload:
             self.units, self.unit = 1, "sweep-steps/s"
             self.desc = "BASELINE configs[2]: one sweep step of the 4096x1024 real SVD"
             self.what = "one full step (512 pairs) per step"
+        elif name in ("step_c64", "dist_c64"):
+            # configs[4]: 16 of the 4096 pairs of a step on CPU-generated columns
+            # of the configs[4] length, in the step kernel's reduction order R
+            # for m = 32768 complex (W = 2048: 8-CTA clusters of 256 threads)
+            rng = np.random.default_rng(5)
+            m, npairs = 32768, 16
+            G = np.asfortranarray((rng.standard_normal((m, 2 * npairs)) +
+                                   1j * rng.standard_normal((m, 2 * npairs))) * 2.0 ** 1000)
+            V = np.asfortranarray(np.eye(2 * npairs, dtype=np.complex128))
+            pairs = np.arange(2 * npairs, dtype=np.int32).reshape(-1, 2)
+            R = O.RSpec.make(2048, 1, [16, 8, 4, 2, 1, 128, 64, 32, 1024, 512, 256])
+            self.fn = lambda: O.step(G, V, pairs, R)
+            self.units, self.unit = npairs / 4096, "sweep-steps/s"
+            self.desc = ("BASELINE configs[4]: complex fp64 Jacobi SVD of one 32768x8192 matrix, "
+                         "one sweep step")
+            self.what = "16 of the 4096 pairs of a step per step (units = fraction of a step)"
+        elif name == "gs_r64":
+            rng = np.random.default_rng(6)
+            m, k = 32768, 64
+            G = rng.standard_normal((m, 2 * k))
+            ef = [O.norm_ef(G[:, j], s=32) for j in range(2 * k)]
+            a = rng.uniform(-1, 1, k)
+
+            def run():
+                for l in range(k):
+                    O.dgsscl(G[:, 2 * l], G[:, 2 * l + 1], ef[2 * l][0], ef[2 * l][1],
+                             ef[2 * l + 1][0], ef[2 * l + 1][1], a[l])
+            self.fn = run
+            self.units, self.unit = k, "pairs/s"
+            self.desc = "NEXT-4 (Alg SM8.1): Gram-Schmidt of g_q against g_p, pairs of 32768 rows"
+            self.what = f"{k} pairs of 32768 rows per step"
         elif name == "norm_c64":
             rng = np.random.default_rng(5)
             cols = rng.standard_normal((32768, 4)) + 1j * rng.standard_normal((32768, 4))

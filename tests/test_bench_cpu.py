@@ -19,7 +19,8 @@ def _lines(out):
     return [json.loads(l) for l in out.splitlines() if l.startswith("{")]
 
 
-@pytest.mark.parametrize("workload", ["evd_c64", "evd_r64", "norm_c64"])
+@pytest.mark.parametrize("workload", ["evd_c64", "evd_r64", "norm_c64", "step_c64", "gs_r64",
+                                      "batched_c64"])
 def test_reference_arm_json_line(workload):
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", workload,
                         "--steps", "1", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True,
