@@ -164,7 +164,8 @@ def test_config3_full_size_step_bitwise(J):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("m,n", [(2, 2), (8, 6), (64, 32), (33, 32), (100, 40), (128, 64)])
+@pytest.mark.parametrize("m,n", [(2, 2), (8, 6), (64, 32), (64, 16), (64, 30), (33, 32), (100, 40),
+                                 (128, 64)])
 def test_gesvj_batched_bitwise(J, cplx, m, n):
     rng = np.random.default_rng(m + n + cplx)
     b = 5
