@@ -125,3 +125,42 @@ def test_gesvj_batched_stays_in_its_matrices(J, cplx):
     for k in range(b):  # the gaps between matrices
         assert bool((abuf[PAD + k * sa + m * n:PAD + (k + 1) * sa] == SENT).all().item())
         assert bool((vbuf[PAD + k * sv + n * n:PAD + (k + 1) * sv] == SENT).all().item())
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_stays_in_its_arrays(J, cplx):
+    m, n, ld = 300, 24, 307
+    dt = torch.complex128 if cplx else torch.float64
+    abuf = torch.full((n * ld + 2 * PAD,), SENT, dtype=dt, device="cuda")
+    A = torch.as_strided(abuf[PAD:], (m, n), (1, ld))
+    A.copy_(torch.randn(n, m, dtype=dt, device="cuda").T)
+    vbuf = torch.full((n * (n + 3) + 2 * PAD,), SENT, dtype=dt, device="cuda")
+    V = torch.as_strided(vbuf[PAD:], (n, n), (1, n + 3))
+    res = J.gesvj(A, V=V, max_sweeps=30)
+    torch.cuda.synchronize()
+    assert res["status"] == 0
+    assert _margins_intact(abuf) and _margins_intact(vbuf)
+    pad_rows = abuf[PAD:PAD + n * ld].view(n, ld)[:, m:]
+    assert bool((pad_rows == SENT).all().item())
+    assert bool((vbuf[PAD:PAD + n * (n + 3)].view(n, n + 3)[:, n:] == SENT).all().item())
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_host_pipeline_stays_in_host_arrays(J, cplx):
+    r = 5000
+    arrs = synth.evd_cfg2(r) if cplx else synth.evd_cfg1(r)
+    ins = [torch.from_numpy(a).pin_memory() for a in arrs] + ([] if cplx else [None])
+    bufs, out = {}, {}
+    for k in ("lam1", "lam2", "cos", "sin_re") + (("sin_im",) if cplx else ()):
+        b = torch.full((r + 2 * PAD,), SENT, dtype=torch.float64).pin_memory()
+        bufs[k], out[k] = b, b[PAD:PAD + r]
+    if not cplx:
+        out["sin_im"] = None
+    for k, n_ in (("zeta", r), ("perm", (r + 31) // 32)):
+        b = torch.full((n_ + 2 * PAD,), -12345, dtype=torch.int32).pin_memory()
+        bufs[k], out[k] = b, b[PAD:PAD + n_]
+    J.evd2_batched_host(*ins, out=out, chunk=1024)
+    torch.cuda.synchronize()
+    for k, b in bufs.items():
+        ref = -12345 if k in ("zeta", "perm") else SENT
+        assert bool((b[:PAD] == ref).all()) and bool((b[-PAD:] == ref).all()), k
