@@ -21,7 +21,7 @@ from ._build import LIB
 
 __all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
            "gesvj_workspace", "gesvj_batched", "launch_count", "evd2_batched_host",
-           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "norm_ef", "dgsscl", "JsvdError", "R64", "C64",
+           "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "gesvj_host", "gesvj_host_workspace", "norm_ef", "dgsscl", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
 
 R64, C64, R32, C32 = 0, 1, 2, 3
@@ -81,6 +81,11 @@ def lib():
         L.jsvd_gesvj_batched_host.restype = ct.c_int
         L.jsvd_gesvj_batched_host.argtypes = ([ct.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
                                                _vp, _vp, _vp, _i64, _vp, ct.c_size_t, _vp])
+        L.jsvd_gesvj_host_workspace.restype = ct.c_int
+        L.jsvd_gesvj_host_workspace.argtypes = [ct.c_int, _i64, _i64, ct.POINTER(ct.c_size_t)]
+        L.jsvd_gesvj_host.restype = ct.c_int
+        L.jsvd_gesvj_host.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _i32, _i32,
+                                      ct.POINTER(_i32), _vp, _vp, ct.c_size_t, _vp]
         L.jsvd_norm_ef.restype = ct.c_int
         L.jsvd_norm_ef.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
         L.jsvd_dgsscl.restype = ct.c_int
@@ -265,6 +270,45 @@ def gesvj_batched_host(A, max_sweeps=30, out=None, chunk=4096, work=None, stream
         _host(out.get("transforms"), "transforms", torch.int64), chunk, _p(work), work.numel(),
         _stream(stream))
     _check(st, "jsvd_gesvj_batched_host")
+    return out
+
+
+def gesvj_host_workspace(cplx, m, n):
+    b = ct.c_size_t()
+    _check(lib().jsvd_gesvj_host_workspace(C64 if cplx else R64, m, n, ct.byref(b)),
+           "jsvd_gesvj_host_workspace")
+    return b.value
+
+
+def gesvj_host(A, nblocks=None, max_sweeps=30, out=None, work=None, stream=None):
+    """jsvd_gesvj on a HOST matrix (jsvd_gesvj_host): A (m x n, column-major
+    host tensor, float64 or complex128) is not modified; returns dict(U, V,
+    sigma, sweeps, tps, status) of host tensors (pinned when allocated here)."""
+    if A.is_cuda or A.dtype not in (torch.float64, torch.complex128) or A.dim() != 2:
+        raise ValueError("A must be a 2-D float64/complex128 HOST tensor")
+    m, n = A.shape
+    if (m > 1 and A.stride(0) != 1) or (n > 1 and A.stride(1) < m):
+        raise ValueError("A must be column-major (use A.T.contiguous().T)")
+    lda = A.stride(1) if n > 1 else m
+    cplx = A.dtype == torch.complex128
+    if out is None:
+        out = dict(U=torch.empty((n, m), dtype=A.dtype, pin_memory=True).T,
+                   V=torch.empty((n, n), dtype=A.dtype, pin_memory=True).T,
+                   sigma=torch.empty(n, dtype=torch.float64, pin_memory=True))
+    wb = gesvj_host_workspace(cplx, m, n)
+    if work is None:
+        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    if not work.is_cuda or work.numel() < wb:
+        raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
+    sw = _i32(0)
+    tps = (_i64 * max(max_sweeps, 1))()
+    st = lib().jsvd_gesvj_host(C64 if cplx else R64, m, n, ct.c_void_p(A.data_ptr()), lda,
+                               ct.c_void_p(out["U"].data_ptr()), ct.c_void_p(out["V"].data_ptr()),
+                               ct.c_void_p(out["sigma"].data_ptr()), n if nblocks is None else nblocks,
+                               max_sweeps, ct.byref(sw), ct.cast(tps, _vp), _p(work), work.numel(),
+                               _stream(stream))
+    _check(st, "jsvd_gesvj_host", allow=(OK, ENOCONV))
+    out.update(sweeps=sw.value, tps=[tps[k] for k in range(sw.value)], status=st)
     return out
 
 

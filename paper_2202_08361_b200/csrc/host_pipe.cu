@@ -223,3 +223,54 @@ extern "C" jsvd_status jsvd_gesvj_batched_host(jsvd_dtype dt, int64_t batch, int
   }
   return join(p, caller) == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
 }
+
+// ---- the full SVD on host buffers: upload, jsvd_gesvj, download ------------
+namespace {
+size_t gesvj_host_parts(bool cplx, int64_t m, int64_t n, size_t* ws) {
+  const size_t w = cplx ? 16 : 8;
+  jsvd_gesvj_workspace(cplx ? JSVD_C64 : JSVD_R64, m, n, ws);
+  return align256(w * m * n) + align256(w * n * n) + align256(8 * n);
+}
+}  // namespace
+
+extern "C" jsvd_status jsvd_gesvj_host_workspace(jsvd_dtype dt, int64_t m, int64_t n,
+                                                 size_t* bytes) {
+  if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || n < 1 || !bytes) return JSVD_EINVAL;
+  size_t ws = 0;
+  const size_t own = gesvj_host_parts(dt == JSVD_C64, m, n, &ws);
+  *bytes = own + ws;
+  return JSVD_OK;
+}
+
+extern "C" jsvd_status jsvd_gesvj_host(jsvd_dtype dt, int64_t m, int64_t n, const double* A,
+                                       int64_t lda, double* U, double* V, double* sigma,
+                                       int32_t nblocks, int32_t max_sweeps, int32_t* sweeps_done,
+                                       int64_t* transforms_per_sweep, void* work,
+                                       size_t work_bytes, void* stream) {
+  if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || n < 1 || lda < m || !A || !U || !V ||
+      !sigma || !work)
+    return JSVD_EINVAL;
+  const bool cplx = dt == JSVD_C64;
+  const size_t w = cplx ? 16 : 8;
+  size_t ws = 0;
+  const size_t own = gesvj_host_parts(cplx, m, n, &ws);
+  if (work_bytes < own + ws) return JSVD_ENOMEM;
+  char* base = static_cast<char*>(work);
+  double* dA = reinterpret_cast<double*>(base);
+  double* dV = reinterpret_cast<double*>(base + align256(w * m * n));
+  double* ds = reinterpret_cast<double*>(base + align256(w * m * n) + align256(w * n * n));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // A (ld = lda on the host) -> packed m x n on the device
+  if (cudaMemcpy2DAsync(dA, w * m, A, w * lda, w * m, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return JSVD_ECUDA;
+  const jsvd_status s = jsvd_gesvj(dt, m, n, dA, m, dV, n, ds, nullptr, nullptr, nblocks,
+                                   max_sweeps, sweeps_done, transforms_per_sweep, base + own, ws,
+                                   stream);
+  if (s != JSVD_OK && s != JSVD_ENOCONV) return s;
+  if (cudaMemcpyAsync(U, dA, w * m * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(V, dV, w * n * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(sigma, ds, 8 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return JSVD_ECUDA;
+  return s;
+}

@@ -134,3 +134,24 @@ def test_gesvj_batched_host_equals_device_path_config4(J):
     for k in ("U", "V", "sigma"):
         assert np.array_equal(_bits(out[k]), _bits(dev[k].cpu())), k
     assert torch.equal(out["transforms"], tr.cpu())
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_host_equals_device_path(J, cplx):
+    rng = np.random.default_rng(12 + cplx)
+    m, n, lda = 300, 24, 305
+    A = rng.standard_normal((m, n)) * 2.0 ** rng.integers(-30, 30, (1, n))
+    if cplx:
+        A = A + 1j * rng.standard_normal((m, n))
+    buf = np.zeros((n, lda), dtype=A.dtype)
+    buf[:, :m] = A.T
+    h = torch.from_numpy(buf).pin_memory().T[:m, :]  # host, column-major, lda = 305
+    out = J.gesvj_host(h, max_sweeps=30)
+    dev = J.gesvj(torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T, max_sweeps=30)
+    torch.cuda.synchronize()
+    assert out["status"] == dev["status"] and out["sweeps"] == dev["sweeps"]
+    assert out["tps"] == dev["tps"]
+    for k in ("U", "V", "sigma"):
+        assert np.array_equal(_bits(out[k].T.contiguous() if k != "sigma" else out[k]),
+                              _bits(dev[k].T.contiguous().cpu() if k != "sigma" else dev[k].cpu())), k
+    assert np.array_equal(h.numpy(), A)  # the host input is not modified
