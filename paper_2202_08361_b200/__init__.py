@@ -177,6 +177,17 @@ def evd2_batched(a11, a22, a21_re, a21_im=None, flags=0, out=None, stream=None):
     return out
 
 
+def _scratch(nbytes, stream):
+    """A device workspace allocated on the current stream for use on `stream`:
+    record_stream keeps the caching allocator from handing the block to other
+    work on the current stream while `stream` (and the library's internal
+    streams, which `stream` joins) may still use it."""
+    work = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    if stream is not None and stream != torch.cuda.current_stream():
+        work.record_stream(stream)
+    return work
+
+
 def _host(t, name, dtype):
     if t is None:
         return None
@@ -219,7 +230,7 @@ def evd2_batched_host(a11, a22, a21_re, a21_im=None, flags=0, out=None, chunk=1 
     ptrs.append(_host(out.get("perm"), "perm", torch.int32))
     wb = evd2_host_workspace(dt, cplx, chunk)
     if work is None:
-        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+        work = _scratch(wb, stream)
     if not work.is_cuda or work.numel() < wb:
         raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
     code = (C64 if cplx else R64) if dt == torch.float64 else (C32 if cplx else R32)
@@ -260,7 +271,7 @@ def gesvj_batched_host(A, max_sweeps=30, out=None, chunk=4096, work=None, stream
             raise ValueError(f"out[{k!r}] must be a host tensor of packed column-major matrices")
     wb = gesvj_batched_host_workspace(cplx, m, n, chunk)
     if work is None:
-        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+        work = _scratch(wb, stream)
     if not work.is_cuda or work.numel() < wb:
         raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
     st = lib().jsvd_gesvj_batched_host(
@@ -297,7 +308,7 @@ def gesvj_host(A, nblocks=None, max_sweeps=30, out=None, work=None, stream=None)
                    sigma=torch.empty(n, dtype=torch.float64, pin_memory=True))
     wb = gesvj_host_workspace(cplx, m, n)
     if work is None:
-        work = torch.empty(wb, dtype=torch.uint8, device="cuda")
+        work = _scratch(wb, stream)
     if not work.is_cuda or work.numel() < wb:
         raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
     sw = _i32(0)

@@ -477,6 +477,14 @@ static int Fm_host(bool cplx, int64_t m) {
   return 1021 - k - (mm >= (static_cast<unsigned __int128>(1) << (2 * k + 1)) ? 1 : 0);
 }
 
+// the shape / dtype conditions of jsvd_gesvj_batched (also checked by the
+// host-buffer entry point before it queues anything)
+bool gesvj_batched_args_ok(jsvd_dtype dt, int64_t m, int64_t n) {
+  if ((dt != JSVD_R64 && dt != JSVD_C64) || m < n || n < 2 || (n & 1) || m > 128 || n > 64)
+    return false;
+  return batched_smem(dt == JSVD_C64, m, n) <= 220 * 1024;
+}
+
 }  // namespace jsvd
 
 using namespace jsvd;
@@ -487,15 +495,13 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                           int32_t max_sweeps, int32_t* sweeps_done,
                                           int32_t* status, int64_t* transforms, void* stream) {
   const bool cplx = dt == JSVD_C64;
-  if ((dt != JSVD_R64 && dt != JSVD_C64) || batch < 0 || m < n || n < 2 || (n & 1) || m > 128 ||
-      n > 64 || lda < m || ldv < n || strideA < lda * n || strideV < ldv * n || max_sweeps < 0 ||
+  if (!gesvj_batched_args_ok(dt, m, n) || batch < 0 || lda < m || ldv < n || strideA < lda * n || strideV < ldv * n || max_sweeps < 0 ||
       !A || !V || !sigma)
     return JSVD_EINVAL;
   if (cplx && ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(V) & 15)))
     return JSVD_EINVAL;
   if (batch == 0) return JSVD_OK;
   const size_t smem = batched_smem(cplx, m, n);
-  if (smem > 220 * 1024) return JSVD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int Fm = Fm_host(cplx, m), Kr = cplx ? 1020 : 1022;
   const double tol = std::ldexp(std::sqrt(static_cast<double>(m)), -53);

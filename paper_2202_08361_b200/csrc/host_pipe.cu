@@ -49,19 +49,34 @@ cudaError_t pipe_streams(PipeStreams** out) {
 }
 
 // internal streams wait for the caller's stream; at the end the caller's
-// stream waits for them
+// stream waits for them.  The shared fork event is recorded and waited on
+// under the lock, so a second host thread cannot re-record it between this
+// call's record and its waits (which would order this call's uploads after
+// the other caller's stream instead of its own).  join's per-stream events
+// are recorded and waited under the lock too; interleaving there could only
+// over-order, but the lock keeps each edge exactly the call's own.
 cudaError_t fork(PipeStreams* p, cudaStream_t caller) {
+  std::lock_guard<std::mutex> g(g_pipe_mu);
   cudaError_t e = cudaEventRecord(p->e[kSlots], caller);
   for (int k = 0; k < kSlots && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(p->s[k], p->e[kSlots], 0);
   return e;
 }
 cudaError_t join(PipeStreams* p, cudaStream_t caller) {
+  std::lock_guard<std::mutex> g(g_pipe_mu);
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < kSlots && e == cudaSuccess; ++k) {
     e = cudaEventRecord(p->e[k], p->s[k]);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, p->e[k], 0);
   }
   return e;
+}
+
+// an error after fork(): the caller's stream still waits for everything the
+// call already queued on the internal streams (e.g. an upload reading the
+// caller's host buffer), so synchronising `stream` stays a sufficient fence
+jsvd_status fail_joined(PipeStreams* p, cudaStream_t caller, jsvd_status st) {
+  join(p, caller);
+  return st;
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -104,6 +119,7 @@ extern "C" jsvd_status jsvd_evd2_batched_host(jsvd_dtype dt, int64_t r, const vo
   const size_t w = f64 ? 8 : 4;
   if (!a11 || !a22 || !a21_re || !lam1 || !lam2 || !cos_phi || !sin_re) return JSVD_EINVAL;
   if (cplx != (a21_im != nullptr) || cplx != (sin_im != nullptr)) return JSVD_EINVAL;
+  if (flags & ~(JSVD_EVD_TAN | JSVD_EVD_NOBACKSCALE)) return JSVD_EINVAL;
   if (r == 0) return JSVD_OK;
   const size_t slot = evd_slot_bytes(cplx, w, chunk);
   if (!work || work_bytes < kSlots * slot) return JSVD_ENOMEM;
@@ -131,7 +147,7 @@ extern "C" jsvd_status jsvd_evd2_batched_host(jsvd_dtype dt, int64_t r, const vo
     for (int j = 0; j < nin; ++j)
       if (cudaMemcpyAsync(din[j], static_cast<const char*>(in[j]) + w * off, nb,
                           cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return JSVD_ECUDA;
+        return fail_joined(p, caller, JSVD_ECUDA);
     jsvd_status st;
     if (f64)
       st = jsvd_evd2_batched(dt, n, reinterpret_cast<const double*>(din[0]),
@@ -151,23 +167,23 @@ extern "C" jsvd_status jsvd_evd2_batched_host(jsvd_dtype dt, int64_t r, const vo
                                  reinterpret_cast<float*>(dout[2]), reinterpret_cast<float*>(dout[3]),
                                  cplx ? reinterpret_cast<float*>(dout[4]) : nullptr,
                                  zeta ? dz : nullptr, perm ? dp : nullptr, flags, s);
-    if (st != JSVD_OK) return st;
+    if (st != JSVD_OK) return fail_joined(p, caller, st);
     for (int j = 0; j < nout; ++j)
       if (cudaMemcpyAsync(static_cast<char*>(out[j]) + w * off, dout[j], nb,
                           cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return JSVD_ECUDA;
+        return fail_joined(p, caller, JSVD_ECUDA);
     if (zeta && cudaMemcpyAsync(zeta + off, dz, 4 * n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
     if (perm && cudaMemcpyAsync(perm + off / 32, dp, 4 * ((n + 31) / 32), cudaMemcpyDeviceToHost,
                                 s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
   }
   return join(p, caller) == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
 }
 
 extern "C" jsvd_status jsvd_gesvj_batched_host_workspace(jsvd_dtype dt, int64_t m, int64_t n,
                                                          int64_t chunk, size_t* bytes) {
-  if (!bytes || chunk < 1 || m < 1 || n < 1 || (dt != JSVD_R64 && dt != JSVD_C64)) return JSVD_EINVAL;
+  if (!bytes || chunk < 1 || !gesvj_batched_args_ok(dt, m, n)) return JSVD_EINVAL;
   *bytes = kSlots * svd_slot_bytes(dt == JSVD_C64, m, n, chunk);
   return JSVD_OK;
 }
@@ -178,8 +194,9 @@ extern "C" jsvd_status jsvd_gesvj_batched_host(jsvd_dtype dt, int64_t batch, int
                                                int32_t* sweeps_done, int32_t* status,
                                                int64_t* transforms, int64_t chunk, void* work,
                                                size_t work_bytes, void* stream) {
-  if ((dt != JSVD_R64 && dt != JSVD_C64) || batch < 0 || chunk < 1 || !A || !U || !V || !sigma)
-    return JSVD_EINVAL;
+  if (batch < 0 || chunk < 1 || !A || !U || !V || !sigma || max_sweeps < 0 ||
+      !gesvj_batched_args_ok(dt, m, n))
+    return JSVD_EINVAL;  // everything jsvd_gesvj_batched checks, before fork()
   if (batch == 0) return JSVD_OK;
   const bool cplx = dt == JSVD_C64;
   const size_t w = cplx ? 16 : 8;
@@ -204,22 +221,22 @@ extern "C" jsvd_status jsvd_gesvj_batched_host(jsvd_dtype dt, int64_t batch, int
     int64_t* dtr = reinterpret_cast<int64_t*>(tail + 2 * align256(8 * chunk));
     if (cudaMemcpyAsync(dA, reinterpret_cast<const char*>(A) + w * m * n * off, w * m * n * nb,
                         cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
     const jsvd_status st = jsvd_gesvj_batched(dt, nb, m, n, dA, m, m * n, dV, n, n * n, ds,
                                               max_sweeps, dsw, dst, dtr, s);
-    if (st != JSVD_OK) return st;
+    if (st != JSVD_OK) return fail_joined(p, caller, st);
     if (cudaMemcpyAsync(reinterpret_cast<char*>(U) + w * m * n * off, dA, w * m * n * nb,
                         cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaMemcpyAsync(reinterpret_cast<char*>(V) + w * n * n * off, dV, w * n * n * nb,
                         cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaMemcpyAsync(sigma + n * off, ds, 8 * n * nb, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
     if (sweeps_done && cudaMemcpyAsync(sweeps_done + off, dsw, 4 * nb, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
     if (status && cudaMemcpyAsync(status + off, dst, 4 * nb, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
     if (transforms && cudaMemcpyAsync(transforms + off, dtr, 8 * nb, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return JSVD_ECUDA;
+      return fail_joined(p, caller, JSVD_ECUDA);
   }
   return join(p, caller) == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
 }

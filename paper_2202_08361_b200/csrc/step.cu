@@ -15,6 +15,7 @@
 // once per transformed pair, nothing for a converged pair (R#26: no max on V).
 #include <mutex>
 #include <vector>
+#include <utility>
 
 #include "jsvd_host.h"
 #include "step_dev.cuh"
@@ -454,17 +455,19 @@ static Geo pick_geo(bool cplx, int64_t m) {
   return Geo{256, static_cast<int>(W / 256), NR, NS};
 }
 
+// kernel attributes (cluster size > 8, > 48 KB dynamic shared memory) are
+// per device: remember (kernel, device) pairs already configured
 static std::mutex g_attr_mu;
-static std::vector<const void*> g_attr_done;
-static bool attrs_done(const void* k) {
+static std::vector<std::pair<const void*, int>> g_attr_done;
+static bool attrs_done(const void* k, int dev) {
   std::lock_guard<std::mutex> g(g_attr_mu);
-  for (const void* p : g_attr_done)
-    if (p == k) return true;
+  for (const auto& p : g_attr_done)
+    if (p.first == k && p.second == dev) return true;
   return false;
 }
-static void mark_attrs_done(const void* k) {
+static void mark_attrs_done(const void* k, int dev) {
   std::lock_guard<std::mutex> g(g_attr_mu);
-  g_attr_done.push_back(k);
+  g_attr_done.emplace_back(k, dev);
 }
 
 template <typename Kern, typename... Args>
@@ -491,9 +494,14 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  // kernel attributes are set once per kernel (not inside a CUDA-graph capture
-  // of later launches)
-  if ((CL > 8 || smem > 48 * 1024) && !attrs_done(reinterpret_cast<const void*>(k))) {
+  // kernel attributes are set once per (kernel, device) (not inside a CUDA-graph
+  // capture of later launches)
+  int dev = 0;
+  if (CL > 8 || smem > 48 * 1024) {
+    cudaError_t a = cudaGetDevice(&dev);
+    if (a != cudaSuccess) return a;
+  }
+  if ((CL > 8 || smem > 48 * 1024) && !attrs_done(reinterpret_cast<const void*>(k), dev)) {
     if (CL > 8) {
       cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (a != cudaSuccess) return a;
@@ -503,7 +511,7 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
                                            static_cast<int>(smem));
       if (a != cudaSuccess) return a;
     }
-    mark_attrs_done(reinterpret_cast<const void*>(k));
+    mark_attrs_done(reinterpret_cast<const void*>(k), dev);
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
   note_launch();

@@ -155,3 +155,60 @@ def test_gesvj_host_equals_device_path(J, cplx):
         assert np.array_equal(_bits(out[k].T.contiguous() if k != "sigma" else out[k]),
                               _bits(dev[k].T.contiguous().cpu() if k != "sigma" else dev[k].cpu())), k
     assert np.array_equal(h.numpy(), A)  # the host input is not modified
+
+
+def test_evd2_host_two_threads_two_streams(J):
+    # the shared fork event must order each call after ITS caller's
+    # stream.  Two host threads, each first writing its pinned inputs from the
+    # device on its own stream (D2H queued just before the call), then calling
+    # the host pipeline on that stream: a call ordered after the other
+    # thread's stream would upload stale inputs.
+    import threading
+    r, chunk = 200003, 8192
+    arrs = [synth.evd_cfg2(r, seed=900 + t) for t in range(2)]
+    refs = [O.evd2_batched(*a, flags=0) for a in arrs]
+    errs = []
+
+    def run(t):
+        try:
+            s = torch.cuda.Stream()
+            dev_in = [torch.from_numpy(a).cuda() for a in arrs[t]]
+            torch.cuda.synchronize()
+            for it in range(4):
+                ins = [torch.full((r,), 3.0, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+                with torch.cuda.stream(s):
+                    for h, d in zip(ins, dev_in):
+                        h.copy_(d, non_blocking=True)
+                out = _host_out(J, r, torch.float64, True, True)
+                J.evd2_batched_host(*ins, out=out, chunk=chunk, stream=s)
+                s.synchronize()
+                _compare(out, refs[t], True, False)
+        except Exception as e:  # surfaced in the main thread
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+
+
+def test_gesvj_batched_host_rejects_shapes_before_queueing(J):
+    # shapes jsvd_gesvj_batched rejects are rejected up front
+    # (nothing queued), by the workspace query and by the call itself
+    import ctypes as ct
+    L = J.lib()
+    work = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    for m, n in ((130, 32), (64, 66), (64, 31), (16, 32)):
+        with pytest.raises(J.JsvdError):
+            J.gesvj_batched_host_workspace(False, m, n, 2)
+        A = torch.zeros(2 * m * n, dtype=torch.float64, pin_memory=True)
+        U = torch.zeros(2 * m * n, dtype=torch.float64, pin_memory=True)
+        V = torch.zeros(2 * n * n, dtype=torch.float64, pin_memory=True)
+        sg = torch.zeros(2 * n, dtype=torch.float64, pin_memory=True)
+        st = L.jsvd_gesvj_batched_host(J.R64, 2, m, n, ct.c_void_p(A.data_ptr()),
+                                       ct.c_void_p(U.data_ptr()), ct.c_void_p(V.data_ptr()),
+                                       ct.c_void_p(sg.data_ptr()), 30, None, None, None, 2,
+                                       ct.c_void_p(work.data_ptr()), work.numel(), None)
+        assert st == -1, (m, n, st)  # JSVD_EINVAL
