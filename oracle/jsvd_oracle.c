@@ -608,13 +608,21 @@ static void scale_matrix(int cplx, int64_t m, int64_t n, double *G, int64_t ldg,
     for (int64_t i = 0; i < w * m; ++i) G[w * j * ldg + i] = scalbn(G[w * j * ldg + i], s);
 }
 
+/* s0_adjust: an integer added to the initial scaling exponent s0 of Eq. (skn)
+ * (0 = the paper's s0 = s_[0]).  Any s0 with a finite G1 is safe: the Eq. (skr)
+ * check at step 0 downscales a G1 that is too large, so a positive adjustment
+ * is the way to make the rescale of P:1071-1115 fire (with the paper's s0 it
+ * cannot: DESIGN.md R#40).  *scale_out (optional) receives the final s, the
+ * effective scaling exponent: G = 2^s (iteration matrix without scaling).   */
 int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V, int64_t ldv,
               double *sigma, double *sigma_e, double *sigma_f, int64_t B, int32_t max_sweeps,
-              int32_t *sweeps_done, int64_t *tps, const orc_rspec *R)
+              int32_t *sweeps_done, int64_t *tps, int32_t s0_adjust, int32_t *scale_out,
+              const orc_rspec *R)
 {
   if (m < n || n < 2 || (n & 1) || lda < m || ldv < n || !rspec_ok(R) || max_sweeps < 0)
     return ORC_EINVAL;
   if (B != n && (n % B || ((n / B) & 1))) return ORC_EINVAL;
+  if (s0_adjust < -2200 || s0_adjust > 2200) return ORC_EINVAL;
   const int64_t w = cplx ? 2 : 1;
   /* line 1: M0, s0, G1 = 2^s0 G0 (Eq. skn) */
   double Mt = maxnorm(cplx, m, n, A, lda);
@@ -622,7 +630,8 @@ int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V,
   if (Mt == 0.0) return ORC_ERANK;
   const int Fm = orc_Fm(cplx, m);
   const int Kr = cplx ? 1020 : 1022; /* floor(lg(omega/varsigma)) [-1]: Eq. skr */
-  int s = Fm - (int)logb(Mt) - 1;
+  int s = Fm - (int)logb(Mt) - 1 + s0_adjust;
+  if ((int)logb(Mt) + s > 1023) return ORC_EINVAL; /* G1 would overflow */
   scale_matrix(cplx, m, n, A, lda, s);
   Mt = scalbn(Mt, s);
   /* line 2: V = I */
@@ -661,10 +670,26 @@ int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V,
     }
   }
   if (sweeps_done) *sweeps_done = C;
-  /* finalize: norms of the final columns.  If converged they
-   * equal those of the last sweep; recomputing them with the same R is
-   * bit-identical and also defines the result for a capped run (R#25).     */
+  if (scale_out) *scale_out = s;
+  /* the column norms of the final iterate, recomputed with the same R (R#23):
+   * if converged they equal those of the last sweep (no column changed). */
   for (int64_t j = 0; j < n; ++j) orc_colnorm(cplx, m, A + w * j * lda, R, &ce[j], &cf[j]);
+  if (!converged) {
+    /* line 41: "if C < S then normalize ..." -- not converged (C = S): A keeps
+     * the iteration matrix G = U Sigma' (scaled by 2^s), V is left as is, and
+     * sigma holds Sigma' = (e_j, f_j), the norms of G's columns in column order,
+     * not backscaled by s and not sorted (R#25).               */
+    for (int64_t j = 0; j < n; ++j) {
+      if (sigma_e) sigma_e[j] = ce[j];
+      if (sigma_f) sigma_f[j] = cf[j];
+      if (sigma) sigma[j] = isinf(ce[j]) ? 0.0 : scalbn(cf[j], (int)ce[j]);
+    }
+    free(ce);
+    free(cf);
+    free(pairs);
+    return ORC_ENOCONV;
+  }
+  /* finalize: u_j = 2^{-e_j} g_j / f_j, e_j = e_j - s */
   for (int64_t j = 0; j < n; ++j) {
     double *g = A + w * j * lda;
     if (!isinf(ce[j])) {
@@ -707,23 +732,24 @@ int orc_gesvj(int cplx, int64_t m, int64_t n, double *A, int64_t lda, double *V,
   free(ce);
   free(cf);
   free(pairs);
-  return converged ? ORC_OK : ORC_ENOCONV;
+  return ORC_OK;
 }
 
 /* A batch of independent SVDs (configuration 4); OpenMP over matrices. */
 int orc_gesvj_batched(int cplx, int64_t batch, int64_t m, int64_t n, double *A, int64_t lda,
                       int64_t strideA, double *V, int64_t ldv, int64_t strideV, double *sigma,
                       int32_t max_sweeps, int32_t *sweeps_done, int32_t *status,
-                      const orc_rspec *R)
+                      int32_t s0_adjust, int32_t *scale_out, const orc_rspec *R)
 {
   const int64_t w = cplx ? 2 : 1;
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < batch; ++b) {
-    int32_t sw = 0;
+    int32_t sw = 0, sc = 0;
     int st = orc_gesvj(cplx, m, n, A + w * b * strideA, lda, V + w * b * strideV, ldv,
-                       sigma + b * n, NULL, NULL, n, max_sweeps, &sw, NULL, R);
+                       sigma + b * n, NULL, NULL, n, max_sweeps, &sw, NULL, s0_adjust, &sc, R);
     if (sweeps_done) sweeps_done[b] = sw;
     if (status) status[b] = st;
+    if (scale_out) scale_out[b] = sc;
   }
   return ORC_OK;
 }

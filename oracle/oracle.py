@@ -98,11 +98,13 @@ def lib():
         L.orc_gesvj.restype = ct.c_int
         L.orc_gesvj.argtypes = [ct.c_int, _I64, _I64, ct.c_void_p, _I64, ct.c_void_p, _I64,
                                 ct.c_void_p, ct.c_void_p, ct.c_void_p, _I64, ct.c_int32,
-                                ct.POINTER(ct.c_int32), ct.c_void_p, ct.POINTER(RSpec)]
+                                ct.POINTER(ct.c_int32), ct.c_void_p, ct.c_int32,
+                                ct.POINTER(ct.c_int32), ct.POINTER(RSpec)]
         L.orc_gesvj_batched.restype = ct.c_int
         L.orc_gesvj_batched.argtypes = [ct.c_int, _I64, _I64, _I64, ct.c_void_p, _I64, _I64,
                                         ct.c_void_p, _I64, _I64, ct.c_void_p, ct.c_int32,
-                                        ct.c_void_p, ct.c_void_p, ct.POINTER(RSpec)]
+                                        ct.c_void_p, ct.c_void_p, ct.c_int32, ct.c_void_p,
+                                        ct.POINTER(RSpec)]
         L.orc_norm_ef.restype = ct.c_int
         L.orc_norm_ef.argtypes = [ct.c_int, _I64, ct.c_void_p, ct.c_int, ct.c_int, _PD, _PD, _PD,
                                   _PD]
@@ -298,8 +300,13 @@ def Fm(cplx, m):
     return lib().orc_Fm(int(cplx), int(m))
 
 
-def gesvj(A, R, B=None, max_sweeps=30):
-    """Full SVD.  A: (m, n) numpy, any order; returns dict with U, V, sigma, ..."""
+def gesvj(A, R, B=None, max_sweeps=30, s0_adjust=0):
+    """Full SVD (Alg 4.1).  A: (m, n) numpy, any order.  Returns dict(U, V,
+    sigma, sigma_e, sigma_f, sweeps, tps, status, scale).  status 0: U
+    normalised, sigma = Sigma sorted (R#24).  status 1 (ENOCONV, C = S): U
+    holds the iteration matrix G = U Sigma' (scaled by 2^scale) and sigma /
+    sigma_e / sigma_f hold Sigma' in column order (R#25).
+    s0_adjust is added to s0 of Eq. (skn) (R#40)."""
     m, n = A.shape
     cplx = np.iscomplexobj(A)
     dt = np.complex128 if cplx else np.float64
@@ -311,17 +318,19 @@ def gesvj(A, R, B=None, max_sweeps=30):
     se = np.zeros(n)
     sf = np.zeros(n)
     sw = ct.c_int32(0)
+    sc = ct.c_int32(0)
     tps = np.zeros(max(max_sweeps, 1), np.int64)
     B = n if B is None else B
     st = lib().orc_gesvj(c, m, n, _ptr(gb), lda, _ptr(vb), ldv, _ptr(sig), _ptr(se), _ptr(sf), B,
-                         max_sweeps, ct.byref(sw), _ptr(tps), ct.byref(R))
+                         max_sweeps, ct.byref(sw), _ptr(tps), int(s0_adjust), ct.byref(sc),
+                         ct.byref(R))
     if st < 0:
         raise ValueError(f"orc_gesvj status {st}")
     return dict(U=G, V=V, sigma=sig, sigma_e=se, sigma_f=sf, sweeps=sw.value,
-                tps=tps[:sw.value], status=st)
+                tps=tps[:sw.value], status=st, scale=sc.value)
 
 
-def gesvj_batched(A, R, max_sweeps=30):
+def gesvj_batched(A, R, max_sweeps=30, s0_adjust=0):
     """A: (batch, m, n) numpy; each matrix column-major in the returned U."""
     b, m, n = A.shape
     cplx = np.iscomplexobj(A)
@@ -332,13 +341,15 @@ def gesvj_batched(A, R, max_sweeps=30):
     sig = np.zeros((b, n))
     sw = np.zeros(b, np.int32)
     st = np.zeros(b, np.int32)
+    sc = np.zeros(b, np.int32)
     gb = G.view(np.float64) if cplx else G
     vb = V.view(np.float64) if cplx else V
     lib().orc_gesvj_batched(int(cplx), b, m, n, _ptr(gb), m, m * n, _ptr(vb), n, n * n,
-                            _ptr(sig), max_sweeps, _ptr(sw), _ptr(st), ct.byref(R))
+                            _ptr(sig), max_sweeps, _ptr(sw), _ptr(st), int(s0_adjust), _ptr(sc),
+                            ct.byref(R))
     U = np.transpose(G, (0, 2, 1))
     Vm = np.transpose(V, (0, 2, 1))
-    return dict(U=U, V=Vm, sigma=sig, sweeps=sw, status=st)
+    return dict(U=U, V=Vm, sigma=sig, sweeps=sw, status=st, scale=sc)
 
 
 def norm_ef(x, s=32, reduction=0):

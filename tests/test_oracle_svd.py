@@ -404,3 +404,147 @@ def test_gesvj_batched_equals_single():
         r = O.gesvj(A[k], R32)
         assert np.array_equal(b["U"][k], r["U"]) and np.array_equal(b["V"][k], r["V"])
         assert np.array_equal(b["sigma"][k], r["sigma"]) and b["sweeps"][k] == r["sweeps"]
+
+
+# ------------------------------------------- non-convergence (Alg 4.1 line 41)
+def test_gesvj_capped_zero_sweeps_returns_scaled_G():
+    # "if C < S then normalize ... ; return C" -- with S = 0 no
+    # sweep runs, C = S, nothing is normalised: A holds G1 = 2^s0 A exactly,
+    # V = I, and (e, f) are the norms of G1's columns, in column order, NOT
+    # backscaled by s.  Hand values: real m = 2: F(2) = floor(lg(omega/4)) =
+    # 1021, M0 = 4 -> s0 = 1021 - 2 - 1 = 1018 (Eq. skn).  Column 1 = 2^1018
+    # (3, 4): E = 1020, y = (3/4, 1), SSQ = 25/16 -> (e, f) = (1020, 5/4);
+    # column 2 = 2^1018 (1, 1): E = 1018, SSQ = 2 (odd exponent) -> g = 2,
+    # (e, f) = (1018, fl(sqrt 2)) (R#14).
+    A = np.array([[3.0, 1.0], [4.0, 1.0]])
+    r = O.gesvj(A, R32, max_sweeps=0)
+    assert r["status"] == 1 and r["sweeps"] == 0 and r["scale"] == 1018
+    assert np.array_equal(r["U"], np.ldexp(A, 1018))
+    assert np.array_equal(r["V"], np.eye(2))
+    assert r["sigma_e"].tolist() == [1020.0, 1018.0]
+    assert r["sigma_f"].tolist() == [1.25, math.sqrt(2.0)]
+    assert r["sigma"].tolist() == [math.ldexp(1.25, 1020), math.ldexp(math.sqrt(2.0), 1018)]
+
+
+def test_gesvj_capped_one_sweep_is_unnormalized_U_sigma():
+    # A = [[1, 1], [0, 1]]: one rotation diagonalises A^T A = [[1,1],[1,2]],
+    # whose eigenvalues are phi^2, phi^-2 (phi the golden ratio), so after the
+    # single sweep (T = 1, not converged, C = S = 1): G = U Sigma' with
+    # orthogonal columns of norms 2^s phi and 2^s / phi (s = F(2) - 0 - 1 =
+    # 1020), G V^T = 2^s A, and sigma' unsorted in column order.
+    A = np.array([[1.0, 1.0], [0.0, 1.0]])
+    phi = (1.0 + math.sqrt(5.0)) / 2.0
+    r = O.gesvj(A, R32, max_sweeps=1)
+    assert r["status"] == 1 and r["sweeps"] == 1 and r["tps"].tolist() == [1]
+    s = r["scale"]
+    assert s == 1020
+    G = np.ldexp(r["U"], -s)
+    V = r["V"]
+    assert abs(G[:, 0] @ G[:, 1]) <= 8 * EPS
+    assert np.linalg.norm(V.T @ V - np.eye(2)) <= 8 * EPS
+    assert np.abs(G @ V.T - A).max() <= 8 * EPS
+    sig = np.ldexp(r["sigma"], -s)
+    assert sorted(sig.tolist(), reverse=True) == pytest.approx([phi, 1 / phi], rel=8 * EPS)
+    for j in range(2):  # not normalised: the columns' norms are sigma'
+        assert np.linalg.norm(G[:, j]) == pytest.approx(sig[j], rel=4 * EPS)
+        assert r["sigma"][j] == math.ldexp(r["sigma_f"][j], int(r["sigma_e"][j]))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_converged_is_normalized_capped_iterate(cplx):
+    # Converged in C sweeps means sweep C had T = 0 and changed nothing, so the
+    # capped run with S = C - 1 ends on the same iteration matrix G: the
+    # converged U must be P:1481-1485's u_j = 2^-e_j g_j / f_j of the capped
+    # G (computed here with numpy's IEEE ldexp and division), sorted by
+    # (e - s, f) descending (R#24), and sigma_e = e - s.
+    A = synth.svd_cfg4(1, m=24, n=12, seed=31)[0]
+    if not cplx:
+        A = np.ascontiguousarray(A.real)
+    conv = O.gesvj(A, R32, max_sweeps=60)
+    C = conv["sweeps"]
+    assert conv["status"] == 0 and C >= 3
+    cap = O.gesvj(A, R32, max_sweeps=C - 1)
+    assert cap["status"] == 1 and cap["sweeps"] == C - 1
+    assert cap["scale"] == conv["scale"]
+    e, f, s = cap["sigma_e"], cap["sigma_f"], cap["scale"]
+    order = sorted(range(12), key=lambda j: (-(e[j] - s), -f[j], j))
+    U = cap["U"]
+    Uexp = np.empty_like(U)
+    for r_, j in enumerate(order):
+        g = U[:, j]
+        if cplx:
+            Uexp[:, r_] = np.ldexp(g.real, -int(e[j])) / f[j] + 1j * (np.ldexp(g.imag, -int(e[j])) / f[j])
+        else:
+            Uexp[:, r_] = np.ldexp(g, -int(e[j])) / f[j]
+    assert np.array_equal(conv["U"], Uexp)
+    assert np.array_equal(conv["V"], cap["V"][:, order])
+    assert np.array_equal(conv["sigma_e"], (e - s)[order])
+    assert np.array_equal(conv["sigma_f"], f[order])
+
+
+# ------------------------------------------ the rescale of Eqs. skn/skr (R#40)
+@pytest.mark.parametrize("a22", [0.0, 2.0 ** -30])
+def test_gesvj_rescale_fires_hand_derived(a22):
+    # Complex m = n = 2: F(2) = 1021 - 1 - [4 >= 8] = 1020, K = 1020 (Eq. skr
+    # fires iff floor(lg M~) >= 1021).  A = [[1.5, 1.5], [0, a22]], M0 = 1.5:
+    # s0 = F - 0 - 1 + adj = 1019 + adj (adj = s0_adjust).  The first rotation
+    # (phi ~ pi/4) maps column 1 to ~ sqrt2 * 1.5 * 2^s0 e1 = 1.06 * 2^(s0+1).
+    #  adj 0: M~1 = 1.5 * 2^1019, after the rotation 1.06 * 2^1020: never fires,
+    #         s = 1019.
+    #  adj 1: M~1 = 1.5 * 2^1020 (no fire at step 0), after the rotation
+    #         1.06 * 2^1021 -> fires at the next check point with
+    #         s_[k] = F - 1021 - 1 = -2: s = 1020 - 2 = 1018.
+    #  adj 2: M~1 = 1.5 * 2^1021 -> fires at step 0, s_[0] = 1020 - 1021 - 1
+    #         = -2: s = 1021 - 2 = 1019, then as adj 0.
+    #  adj 3: floor(lg M~1) = 1022 -> s_[0] = -3: s = 1019.
+    # Scaling by powers of two is exact here (no subnormals, no overflow), so
+    # U, V, sigma (backscaled by s) are bitwise those of adj 0.
+    A = np.array([[1.5, 1.5], [0.0, a22]], dtype=np.complex128)
+    ref = O.gesvj(A, R32)
+    assert ref["status"] == 0 and ref["scale"] == 1019
+    for adj, s in ((1, 1018), (2, 1019), (3, 1019)):
+        r = O.gesvj(A, R32, s0_adjust=adj)
+        assert r["scale"] == s, adj
+        for k in ("U", "V", "sigma", "sigma_e", "sigma_f"):
+            assert np.array_equal(r[k], ref[k]), (adj, k)
+        assert r["sweeps"] == ref["sweeps"] and np.array_equal(r["tps"], ref["tps"])
+    with pytest.raises(ValueError):  # G1 would overflow
+        O.gesvj(A, R32, s0_adjust=5)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_rescale_fires_mid_run_random(cplx):
+    # s0_adjust = K + 1 - F(m) starts the iteration with floor(lg M~1) = K
+    # (K = 1022 real, 1020 complex), so the check fires at the first check
+    # point after some component reaches 2^(K+1).  Every rescale is a power
+    # of two: the result equals the unadjusted run bitwise, and the final s
+    # tells how far the iteration was scaled down.
+    rng = np.random.default_rng(7 + cplx)
+    K = 1020 if cplx else 1022
+    fired = 0
+    for t in range(24):
+        m = int(rng.integers(2, 7))
+        n = 2 * int(rng.integers(1, m // 2 + 1))
+        A = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cplx else 0)
+        ref = O.gesvj(A, R32, B=n)
+        adj = K + 1 - O.Fm(cplx, m)
+        r = O.gesvj(A, R32, B=n, s0_adjust=adj)
+        s_start = ref["scale"] + adj
+        assert r["scale"] <= s_start
+        fired += r["scale"] < s_start
+        for k in ("U", "V", "sigma", "sigma_e", "sigma_f"):
+            assert np.array_equal(r[k], ref[k]), (t, k)
+        # after a rescale floor(lg M~) = F - 1, i.e. the iteration is back at
+        # the paper's scale or below it
+        if r["scale"] < s_start:
+            assert r["scale"] <= ref["scale"]
+    assert fired >= 4  # deterministic seeds: 5 (complex) of 24 fire
+
+
+def test_gesvj_batched_passes_s0_adjust_and_scale():
+    A = synth.svd_cfg4(3, m=8, n=4, seed=41)
+    adj = 1021 - O.Fm(True, 8)
+    b = O.gesvj_batched(A, R32, s0_adjust=adj)
+    for k in range(3):
+        r = O.gesvj(A[k], R32, s0_adjust=adj)
+        assert np.array_equal(b["U"][k], r["U"]) and b["scale"][k] == r["scale"]
