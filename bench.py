@@ -5,9 +5,12 @@ Default workload (N=1): BASELINE.json configs[1], the batched complex 2x2
 Hermitian EVD of r = 2^26 matrices (jsvd_evd2_batched).  One "step" = one
 pass of the EVD over the whole batch with inputs resident in HBM (5.1 GB of
 algorithmic traffic per step, > L2, so no L2 flush is needed).  Multi-GPU: one
-process per GPU (torchrun); every rank runs its own 2^26-matrix shard of a
-global batch (counter-based inputs: shard k == slice k of the whole batch) --
-"scaling": "weak", no data-path collective (the batch shards naturally).
+process per GPU (torchrun); the configured batch is split by batch index, rank
+k runs matrices [k r/N, (k+1) r/N) (counter-based inputs: shard k == slice k of
+the whole batch) -- "scaling": "strong" (the total work is the configured
+batch at every N), no data-path collective (the batch shards naturally,
+SURVEY 8(e)).  dist_c64 splits configs[4]'s one SVD by column blocks (the
+library's NCCL exchange), also strong scaling.
 
 Other workloads (--workload, one JSON line each):
   evd_r64      configs[0]  batched real EVD, r = 2^20 (L2-resident: flushed per step)
@@ -15,6 +18,9 @@ Other workloads (--workload, one JSON line each):
   gesvj_r64    configs[2]  the full SVD (<= 30 sweeps), sweep-steps/s
   batched_c64  configs[3]  65536 complex 64 x 32 SVDs, SVD/s
   step_c64     configs[4]  one sweep step of the complex 32768 x 8192 SVD (1 GPU)
+  dist_c64     configs[4]  jsvd_gesvj sharded by column blocks over the torchrun
+                           ranks (NCCL send/recv inside libjsvd), bounded to the
+                           first 1024 sweep steps per bench step (one block exchange)
 
 --impl reference: the oracle (oracle/, plain C) on this box's host cores, on a
 bounded sample of the same workload per step (this tier's reference arm).
@@ -54,7 +60,8 @@ def load_traffic(workload):
 
 # --------------------------------------------------------------- clocks sampler
 class ClockSampler:
-    """Samples SM clock + throttle reasons via NVML every ~20 ms while active."""
+    """Samples SM clock + throttle reasons via NVML every ~1 ms while active
+    (a 1 ms EVD step sees about one sample per launch)."""
 
     def __init__(self, dev_index):
         self.samples, self.reasons, self.max_mhz = [], set(), None
@@ -85,7 +92,7 @@ class ClockSampler:
                                 self.reasons.add(k)
                     except Exception:
                         pass
-                    time.sleep(0.02)
+                    time.sleep(0.001)
 
             self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
@@ -114,12 +121,12 @@ def _ncores():
 # --------------------------------------------------------------- workloads
 # workload descriptions shared by both arms (config.workload of the JSON line)
 DESC = {
-    "evd_c64": "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 per GPU, seed 7",
-    "evd_r64": "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 per GPU, seed 42",
+    "evd_c64": "BASELINE configs[1]: batched complex Hermitian 2x2 EVD, fp64, r=2^26 (split over the GPUs), seed 7",
+    "evd_r64": "BASELINE configs[0]: batched real symmetric 2x2 EVD, fp64, r=2^20 (split over the GPUs), seed 42",
     "evd_c32": ("single-precision analogue of BASELINE configs[1] (NEXT-1, P:709-717): "
-                "batched complex Hermitian 2x2 EVD, fp32, r=2^26 per GPU, seed 7"),
-    "batched_c64": ("BASELINE configs[3]: batch of 65536 complex fp64 64x32 matrices, "
-                    "re,im ~ N(0,1), full Jacobi SVD (U, Sigma, V) of each, seed 4"),
+                "batched complex Hermitian 2x2 EVD, fp32, r=2^26 (split over the GPUs), seed 7"),
+    "batched_c64": ("BASELINE configs[3]: batch of 65536 complex fp64 64x32 matrices (split over "
+                    "the GPUs), re,im ~ N(0,1), full Jacobi SVD (U, Sigma, V) of each, seed 4"),
     "norm_c64": ("NEXT-3 (Alg SM6.3): one-pass (e,f) Frobenius norms of the 8192 columns of "
                  "BASELINE configs[4]'s complex fp64 32768x8192 matrix, s = 32 lanes"),
 }
@@ -135,23 +142,25 @@ class EvdWorkload:
         self.name = name
         self.cplx = name in ("evd_c64", "evd_c32")
         self.f32 = name == "evd_c32"
-        self.r = (1 << 26) if self.cplx else (1 << 20)
+        self.r_total = (1 << 26) if self.cplx else (1 << 20)
+        self.r = self.r_total // world  # this rank's shard of the configured batch
         self.unit = "EVD/s"
+        off = rank * self.r
         if self.f32:
             self.desc = DESC["evd_c32"]
-            self.host = synth.evd_cfg2_f32(self.r, off=rank * self.r)
+            self.host = synth.evd_cfg2_f32(self.r, off=off)
         elif self.cplx:
             self.desc = DESC["evd_c64"]
-            self.host = synth.evd_cfg2(self.r, off=rank * self.r)
+            self.host = synth.evd_cfg2(self.r, off=off)
         else:
             self.desc = DESC["evd_r64"]
-            self.host = synth.evd_cfg1(self.r, off=rank * self.r)
+            self.host = synth.evd_cfg1(self.r, off=off)
         w = 4 if self.f32 else 8
         self.unit_bytes = (9 * w + 4 + 1 / 8) if self.cplx else (7 * w + 4 + 1 / 8)
         fdt = torch.float32 if self.f32 else torch.float64
-        # configs[0] is 63 MB (< 126 MB L2): the steps cycle through 4 separate
-        # input/output sets (252 MB > L2), so every launch streams from HBM
-        self.nsets = 1 if self.cplx else 4
+        # configs[0] is 63 MB (< 126 MB L2): the steps cycle through separate
+        # input/output sets (> 252 MB in all, > L2), so every launch streams from HBM
+        self.nsets = 1 if self.cplx else 4 * world
         keys = ("lam1", "lam2", "cos", "sin_re") + (("sin_im",) if self.cplx else ())
         self.sets = []
         for _ in range(self.nsets):
@@ -166,9 +175,10 @@ class EvdWorkload:
         self.k = 0
         self.units_per_step = self.r
         self.kernel = "evd2f_vec4_kernel" if self.f32 else ("evd2_vec2_kernel" if self.cplx else "evd2_scalar_kernel")
-        self.l2_note = ("inputs+outputs %.1f GB per step > 126 MB L2 (no flush needed)"
+        self.l2_note = ("inputs+outputs %.1f GB per step per GPU > 126 MB L2 (no flush needed)"
                         % (self.unit_bytes * self.r / 1e9)) if self.cplx else \
-            "63 MB per step; steps cycle through 4 input/output sets (252 MB > 126 MB L2)"
+            ("%.0f MB per step per GPU; steps cycle through %d input/output sets (%.0f MB > 126 MB L2)"
+             % (self.unit_bytes * self.r / 1e6, self.nsets, self.nsets * self.unit_bytes * self.r / 1e6))
 
     def prepare(self):
         pass
@@ -312,7 +322,7 @@ class BatchedWorkload:
         import torch
         import synth
         self.name, self.unit = name, "SVD/s"
-        self.b, self.m, self.n = 65536, 64, 32
+        self.b, self.m, self.n = 65536 // world, 64, 32  # this rank's shard
         self.desc = DESC["batched_c64"]
         self.host = synth.svd_cfg4(self.b, off=rank * self.b)
         self.A0 = torch.from_numpy(np.ascontiguousarray(np.transpose(self.host, (0, 2, 1)))).cuda()
@@ -528,76 +538,84 @@ class StepC64Workload(StepWorkload):
 
 
 class DistC64Workload:
-    """configs[4] column-block sharded over the torchrun ranks (N = 1, 2, 4, 8):
-    paper_2202_08361_b200.dist with NCCL send/recv block exchange; one bench
-    step = one global sweep step (4096 pairs over all ranks); the timed window
-    straddles the first phase-II round's block exchange."""
+    """configs[4] sharded by column blocks over the torchrun ranks (N = 1, 2, 4,
+    8): jsvd_gesvj with a jsvd_dist (the library's own NCCL communicator,
+    bootstrapped over the torch.distributed group; N = 1: a one-rank NCCL
+    world, block moves as device copies).  One bench step = one jsvd_gesvj call
+    bounded to the first 2b = 1024 sweep steps (opts.max_steps): phase I (511
+    steps, no exchange), the first phase-II round (512 steps) with its block
+    exchange, and the first step of the next round; the local columns are
+    restored from a pristine copy before each call (untimed).  The unit is the
+    global sweep step (4096 pairs over all ranks)."""
 
     def __init__(self, name, rank, world):
         import torch
         import synth
-        from paper_2202_08361_b200.dist import (BlockSchedule, CudaCompute, DistJacobi,
-                                                LocalRanks, TorchDistRanks, scatter_columns)
+        from paper_2202_08361_b200.dist import NcclDist, local_columns
         self.name, self.unit = name, "sweep-steps/s"
         self.desc = ("BASELINE configs[4]: complex fp64 Jacobi SVD of one 32768x8192 matrix, "
-                     f"column blocks (B=16) sharded over {world} GPU(s), NCCL block exchange")
+                     f"column blocks (B=16) sharded over {world} GPU(s), NCCL block exchange "
+                     "inside libjsvd, the first 1024 sweep steps per call")
         A, _ = synth.svd_cfg5_torch()
         self.m, self.n = A.shape
-        self.S = BlockSchedule(self.n, 16, world)
-        cols = torch.from_numpy(scatter_columns(None, self.S, rank)).cuda()
-        Gt = A.T[cols].contiguous()  # (ncols_local, m)
+        self.B = 16
+        cols = torch.from_numpy(local_columns(self.n, self.B, rank, world)).cuda()
+        self.A0 = A.T[cols].contiguous()  # (n/N, m): the local columns, column-major
         del A
         torch.cuda.empty_cache()
-        ranks = TorchDistRanks() if world > 1 else LocalRanks(1)
-        self.D = DistJacobi([Gt], self.S, ranks, CudaCompute(), cplx=True)
-        self.D.begin_sweep()
-        self.k = 0
+        self.At = torch.empty_like(self.A0)
+        self.V = torch.empty((self.A0.shape[0], self.n), dtype=torch.complex128, device="cuda")
+        self.nd = NcclDist() if world > 1 else NcclDist.single(flags=0)
+        import paper_2202_08361_b200 as J
+        self.work = torch.empty(J.gesvj_workspace(True, self.m, self.n, self.B, self.nd.dist),
+                                dtype=torch.uint8, device="cuda")
+        self.max_steps = 2 * (self.n // self.B)
         self.world = world
-        self.units_per_step = 1.0 / world  # value = world * units * steps / time = global steps/s
+        self.units_per_step = self.max_steps / world  # value = world * units * K / t = global steps/s
         self.kernel = "step_kernel<1,256,8,4,12>"
-        self.l2_note = "local G + V >> L2"
+        self.l2_note = "local G + V >> L2; local columns restored before each call (untimed)"
+        self.last = None
 
     def prepare(self):
-        pass
-
-    def skip_to(self, k0):
-        while self.k < k0:
-            self.step(None)
-
-    def reset_counters(self):
-        pass
+        self.At.copy_(self.A0)
 
     def step(self, stream):
-        self.D.step(self.k)
-        self.k += 1
+        import paper_2202_08361_b200 as J
+        self.last = J.gesvj(self.At.T, nblocks=self.B, max_sweeps=1, V=self.V.T, work=self.work,
+                            stream=stream, dist=self.nd.dist, n=self.n, max_steps=self.max_steps)
 
-    def bytes_for(self, steps, transformed):
+    def bytes_per_step(self):
+        """per-GPU algorithmic bytes of one call: every pair of the first sweep
+        transforms (read + write G pair, read + write V pair)."""
         w = 16
-        return transformed * (4 * self.m * w + 4 * self.n * w)
+        pairs = self.max_steps * (self.n // 2) // self.world
+        return pairs * (4 * self.m * w + 4 * self.n * w)
 
     def e2e(self, stream, steps):
-        """local blocks in from pinned host memory, `steps` steps, local G and V back out."""
+        """local columns in from pinned host memory, one bounded call, local U
+        (iterate) and V back out."""
         import torch
-        Gt, Vt = self.D.Gts[0], self.D.Vts[0]
-        hG = Gt.cpu().pin_memory()
-        hV = torch.empty(Vt.shape, dtype=Vt.dtype).pin_memory()
+        import paper_2202_08361_b200 as J
+        hA = self.A0.cpu().pin_memory()
+        hV = torch.empty(self.V.shape, dtype=self.V.dtype).pin_memory()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        self.D.Gts[0].copy_(hG, non_blocking=True)
         for _ in range(steps):
-            self.step(stream)
-        hG.copy_(self.D.Gts[0], non_blocking=True)
-        hV.copy_(self.D.Vts[0], non_blocking=True)
+            self.At.copy_(hA, non_blocking=True)
+            J.gesvj(self.At.T, nblocks=self.B, max_sweeps=1, V=self.V.T, work=self.work,
+                    stream=stream, dist=self.nd.dist, n=self.n, max_steps=self.max_steps)
+            hA.copy_(self.At, non_blocking=True)
+            hV.copy_(self.V, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1), hG.numel() * 16, (hG.numel() + hV.numel()) * 16
+        self.e2e_note = "jsvd_gesvj (sharded, max_steps 1024) between pinned host copies of the local columns"
+        return e0.elapsed_time(e1), hA.numel() * 16, (hA.numel() + hV.numel()) * 16
 
     def cpu_sample(self):
         import oracle as O
-        import paper_2202_08361_b200 as J
-        R = O.RSpec.make(*J.step_rspec(True, self.m))
+        R = O.RSpec.make(2048, 1, [16, 8, 4, 2, 1, 128, 64, 32, 1024, 512, 256])  # R#15, m = 32768
         npairs = 16
-        G = np.asfortranarray(self.D.Gts[0][: 2 * npairs].cpu().numpy().T)
+        G = np.asfortranarray(self.A0[: 2 * npairs].cpu().numpy().T)
         V = np.asfortranarray(np.eye(2 * npairs, dtype=np.complex128))
         pairs = np.arange(2 * npairs, dtype=np.int32).reshape(-1, 2)
         return (lambda: O.step(G, V, pairs, R)), npairs / (self.n // 2), \
@@ -773,7 +791,7 @@ def run_jsvd(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.workload](args.workload, rank, world)
     stream = torch.cuda.current_stream()
-    per_step_events = args.workload in ("batched_c64", "gesvj_r64")
+    per_step_events = args.workload in ("batched_c64", "gesvj_r64", "dist_c64")
 
     for _ in range(args.warmup):
         wl.prepare()
@@ -781,9 +799,6 @@ def run_jsvd(args):
     torch.cuda.synchronize()
     if hasattr(wl, "reset_counters"):
         wl.reset_counters()
-    if hasattr(wl, "skip_to"):  # dist: let the timed window straddle a block exchange
-        wl.skip_to(max(wl.k, 2 * wl.S.b - 1 - args.steps // 2))
-        torch.cuda.synchronize()
     # steps that are pure asynchronous launches (no host sync, no per-step
     # preparation) are captured once as a CUDA graph of exactly K steps and
     # timed as one replay: the device time of the K launches without the
@@ -860,9 +875,9 @@ def run_jsvd(args):
         bytes_step = wl.bytes_for(args.steps, transformed) / args.steps
         extra["transformed_pairs_per_step"] = transformed / args.steps
     elif isinstance(wl, DistC64Workload):  # per-GPU share; first sweep: every pair transforms
-        bytes_step = wl.bytes_for(1, wl.n // 2) / world
-        extra.update(scaling_note="strong: one SVD, columns sharded", first_step_timed=wl.k - args.steps,
-                     exchange_after_step=2 * wl.S.b - 2)
+        bytes_step = wl.bytes_per_step()
+        extra.update(sweep_steps_per_call=wl.max_steps, exchange_after_step=wl.max_steps - 2,
+                     transforms_first_sweep=wl.last["tps"], status=wl.last["status"])
     else:
         bytes_step = wl.bytes_per_step()
     achieved = bytes_step / (ms_per_step / 1e3) / 1e9
@@ -875,7 +890,11 @@ def run_jsvd(args):
         extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
     if isinstance(wl, GesvjWorkload):
         extra.update(extra_g)
+        # capped (ENOCONV): sigma holds Sigma' in column order,
+        # Sigma = 2^-scale Sigma' sorted; converged: sigma sorted already
         s = wl.last["sigma"].cpu().numpy()
+        if wl.last["status"] != 0:
+            s = np.sort(np.ldexp(s, -wl.last["scale"]))[::-1]
         extra["sigma_err_normwise"] = float(np.abs(s - wl.sig_true).max() / wl.sig_true[0])
     if isinstance(wl, BatchedWorkload):
         sw = wl.sw.float().mean().item()
@@ -936,7 +955,7 @@ def run_jsvd(args):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32" if getattr(wl, "f32", False) else "f64",
             "data": "synthetic (counter-based SplitMix64, DESIGN.md recipe)",
@@ -944,7 +963,10 @@ def run_jsvd(args):
                        "timing": ("one CUDA-graph replay of the K steps (CUDA events)" if graph is not None
                                   else "per-step CUDA events" if per_step_events else
                                   "CUDA events around K launches"),
-                       "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+                       "parallelism": (("column-block shard x%d (B=16, NCCL send/recv in libjsvd)" % world)
+                                       if isinstance(wl, DistC64Workload) else
+                                       ("batch-index shard x%d of the configured batch" % world))
+                       if world > 1 else "single GPU",
                        "l2": wl.l2_note},
             "e2e": {"value": e2e_val, "unit": wl.unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
@@ -1024,7 +1046,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": wl.unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if args.workload == "evd_c32" else "f64",
         "data": "synthetic",
         "config": {"workload": wl.desc, "sample_per_step": wl.what},

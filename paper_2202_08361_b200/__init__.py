@@ -19,7 +19,8 @@ import torch
 
 from ._build import LIB
 
-__all__ = ["lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
+__all__ = ["Dist", "Transport", "GesvjOpts", "DIST_SELF_P2P", "nccl_unique_id", "nccl_comm_init",
+           "nccl_comm_destroy", "dist_columns", "dist_local_pairs", "lib", "evd2_batched", "sweep_step", "step_rspec", "batched_rspec", "strategy_pairs", "gesvj",
            "gesvj_workspace", "gesvj_batched", "launch_count", "evd2_batched_host",
            "evd2_host_workspace", "gesvj_batched_host", "gesvj_batched_host_workspace", "gesvj_host", "gesvj_host_workspace", "norm_ef", "dgsscl", "JsvdError", "R64", "C64",
            "EVD_TAN", "EVD_NOBACKSCALE", "ZETA_ZERO", "status_string"]
@@ -38,6 +39,29 @@ class JsvdError(RuntimeError):
 
 _lib = None
 _vp, _i64, _i32, _d = ct.c_void_p, ct.c_int64, ct.c_int32, ct.c_double
+
+# jsvd_transport callbacks (include/jsvd.h): host-staged sendrecv / allreduce / allgather
+SENDRECV_FN = ct.CFUNCTYPE(ct.c_int, _vp, _i32, ct.POINTER(_i32), ct.POINTER(_i32),
+                           ct.POINTER(_vp), ct.POINTER(_i64))
+ALLREDUCE_FN = ct.CFUNCTYPE(ct.c_int, _vp, _vp, _i32, _i32)
+ALLGATHER_FN = ct.CFUNCTYPE(ct.c_int, _vp, _vp, _vp, _i64)
+
+
+class Transport(ct.Structure):
+    _fields_ = [("ctx", _vp), ("sendrecv", SENDRECV_FN), ("allreduce", ALLREDUCE_FN),
+                ("allgather", ALLGATHER_FN)]
+
+
+class Dist(ct.Structure):
+    _fields_ = [("nccl_comm", _vp), ("rank", _i32), ("nranks", _i32),
+                ("xport", ct.POINTER(Transport)), ("flags", ct.c_uint32)]
+
+
+class GesvjOpts(ct.Structure):
+    _fields_ = [("s0_adjust", _i32), ("max_steps", _i32)]
+
+
+DIST_SELF_P2P = 0x1
 
 
 def lib():
@@ -63,13 +87,26 @@ def lib():
         L.jsvd_strategy_pairs.restype = ct.c_int
         L.jsvd_strategy_pairs.argtypes = [_i64, _i32, _i64, _vp, _vp]
         L.jsvd_gesvj_workspace.restype = ct.c_int
-        L.jsvd_gesvj_workspace.argtypes = [ct.c_int, _i64, _i64, ct.POINTER(ct.c_size_t)]
+        L.jsvd_gesvj_workspace.argtypes = [ct.c_int, _i64, _i64, _i32, ct.POINTER(Dist),
+                                           ct.POINTER(ct.c_size_t)]
         L.jsvd_gesvj.restype = ct.c_int
-        L.jsvd_gesvj.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i32,
-                                 _i32, ct.POINTER(_i32), _vp, _vp, ct.c_size_t, _vp]
+        L.jsvd_gesvj.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
+                                 _i32, _i32, ct.POINTER(_i32), _vp, ct.POINTER(_i32),
+                                 ct.POINTER(GesvjOpts), _vp, ct.c_size_t, ct.POINTER(Dist), _vp]
         L.jsvd_gesvj_batched.restype = ct.c_int
         L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
-                                         _i64, _vp, _i32, _vp, _vp, _vp, _vp]
+                                         _i64, _vp, _i32, _vp, _vp, _vp, _vp,
+                                         ct.POINTER(GesvjOpts), _vp]
+        L.jsvd_nccl_unique_id.restype = ct.c_int
+        L.jsvd_nccl_unique_id.argtypes = [_vp]
+        L.jsvd_nccl_comm_init.restype = ct.c_int
+        L.jsvd_nccl_comm_init.argtypes = [ct.POINTER(_vp), _i32, _vp, _i32]
+        L.jsvd_nccl_comm_destroy.restype = ct.c_int
+        L.jsvd_nccl_comm_destroy.argtypes = [_vp]
+        L.jsvd_dist_columns.restype = ct.c_int
+        L.jsvd_dist_columns.argtypes = [_i64, _i32, _i32, _i32, _vp]
+        L.jsvd_dist_local_pairs.restype = ct.c_int
+        L.jsvd_dist_local_pairs.argtypes = [_i64, _i32, _i32, _i32, _i64, _vp]
         L.jsvd_evd2_host_workspace.restype = ct.c_int
         L.jsvd_evd2_host_workspace.argtypes = [ct.c_int, _i64, ct.POINTER(ct.c_size_t)]
         L.jsvd_evd2_batched_host.restype = ct.c_int
@@ -82,10 +119,10 @@ def lib():
         L.jsvd_gesvj_batched_host.argtypes = ([ct.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
                                                _vp, _vp, _vp, _i64, _vp, ct.c_size_t, _vp])
         L.jsvd_gesvj_host_workspace.restype = ct.c_int
-        L.jsvd_gesvj_host_workspace.argtypes = [ct.c_int, _i64, _i64, ct.POINTER(ct.c_size_t)]
+        L.jsvd_gesvj_host_workspace.argtypes = [ct.c_int, _i64, _i64, _i32, ct.POINTER(ct.c_size_t)]
         L.jsvd_gesvj_host.restype = ct.c_int
         L.jsvd_gesvj_host.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _i32, _i32,
-                                      ct.POINTER(_i32), _vp, _vp, ct.c_size_t, _vp]
+                                      ct.POINTER(_i32), _vp, ct.POINTER(_i32), _vp, ct.c_size_t, _vp]
         L.jsvd_norm_ef.restype = ct.c_int
         L.jsvd_norm_ef.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
         L.jsvd_dgsscl.restype = ct.c_int
@@ -284,9 +321,10 @@ def gesvj_batched_host(A, max_sweeps=30, out=None, chunk=4096, work=None, stream
     return out
 
 
-def gesvj_host_workspace(cplx, m, n):
+def gesvj_host_workspace(cplx, m, n, nblocks=None):
     b = ct.c_size_t()
-    _check(lib().jsvd_gesvj_host_workspace(C64 if cplx else R64, m, n, ct.byref(b)),
+    _check(lib().jsvd_gesvj_host_workspace(C64 if cplx else R64, m, n,
+                                           n if nblocks is None else nblocks, ct.byref(b)),
            "jsvd_gesvj_host_workspace")
     return b.value
 
@@ -294,7 +332,8 @@ def gesvj_host_workspace(cplx, m, n):
 def gesvj_host(A, nblocks=None, max_sweeps=30, out=None, work=None, stream=None):
     """jsvd_gesvj on a HOST matrix (jsvd_gesvj_host): A (m x n, column-major
     host tensor, float64 or complex128) is not modified; returns dict(U, V,
-    sigma, sweeps, tps, status) of host tensors (pinned when allocated here)."""
+    sigma, sweeps, tps, status, scale) of host tensors (pinned when allocated
+    here)."""
     if A.is_cuda or A.dtype not in (torch.float64, torch.complex128) or A.dim() != 2:
         raise ValueError("A must be a 2-D float64/complex128 HOST tensor")
     m, n = A.shape
@@ -306,20 +345,21 @@ def gesvj_host(A, nblocks=None, max_sweeps=30, out=None, work=None, stream=None)
         out = dict(U=torch.empty((n, m), dtype=A.dtype, pin_memory=True).T,
                    V=torch.empty((n, n), dtype=A.dtype, pin_memory=True).T,
                    sigma=torch.empty(n, dtype=torch.float64, pin_memory=True))
-    wb = gesvj_host_workspace(cplx, m, n)
+    nb = n if nblocks is None else nblocks
+    wb = gesvj_host_workspace(cplx, m, n, nb)
     if work is None:
         work = _scratch(wb, stream)
     if not work.is_cuda or work.numel() < wb:
         raise ValueError(f"work must be a CUDA uint8 tensor of >= {wb} bytes")
-    sw = _i32(0)
+    sw, sc = _i32(0), _i32(0)
     tps = (_i64 * max(max_sweeps, 1))()
     st = lib().jsvd_gesvj_host(C64 if cplx else R64, m, n, ct.c_void_p(A.data_ptr()), lda,
                                ct.c_void_p(out["U"].data_ptr()), ct.c_void_p(out["V"].data_ptr()),
-                               ct.c_void_p(out["sigma"].data_ptr()), n if nblocks is None else nblocks,
-                               max_sweeps, ct.byref(sw), ct.cast(tps, _vp), _p(work), work.numel(),
+                               ct.c_void_p(out["sigma"].data_ptr()), nb, max_sweeps, ct.byref(sw),
+                               ct.cast(tps, _vp), ct.byref(sc), _p(work), work.numel(),
                                _stream(stream))
     _check(st, "jsvd_gesvj_host", allow=(OK, ENOCONV))
-    out.update(sweeps=sw.value, tps=[tps[k] for k in range(sw.value)], status=st)
+    out.update(sweeps=sw.value, tps=[tps[k] for k in range(sw.value)], status=st, scale=sc.value)
     return out
 
 
@@ -458,44 +498,66 @@ def normalize(G, col_e, col_f, stream=None):
     return G
 
 
-def gesvj_workspace(cplx, m, n):
+def _opts(s0_adjust, max_steps=0):
+    return ct.byref(GesvjOpts(int(s0_adjust), int(max_steps))) if (s0_adjust or max_steps) else None
+
+
+def gesvj_workspace(cplx, m, n, nblocks=None, dist=None):
     b = ct.c_size_t()
-    _check(lib().jsvd_gesvj_workspace(C64 if cplx else R64, m, n, ct.byref(b)),
+    _check(lib().jsvd_gesvj_workspace(C64 if cplx else R64, m, n, n if nblocks is None else nblocks,
+                                      ct.byref(dist) if dist is not None else None, ct.byref(b)),
            "jsvd_gesvj_workspace")
     return b.value
 
 
-def gesvj(A, nblocks=None, max_sweeps=30, V=None, work=None, stream=None):
-    """Full SVD in place: A (column-major m x n) becomes U.  Returns dict."""
+def gesvj(A, nblocks=None, max_sweeps=30, V=None, work=None, stream=None, s0_adjust=0,
+          dist=None, n=None, max_steps=0, out=None):
+    """Alg 4.1 in place: A (column-major m x ncols) becomes U (converged) or
+    G = U Sigma' (status ENOCONV).  Returns dict(U, V, sigma,
+    sigma_e, sigma_f, perm, sweeps, tps, status, scale).
+
+    dist (a Dist struct, see dist.py): this rank's columns of a sharded SVD of
+    order n (A: m x n/nranks packed, V: n x n/nranks); sigma / perm are the
+    global sorted values, U and V stay distributed.  max_steps > 0 stops after
+    that many steps (timing a bounded run: ENOCONV, no finalize)."""
     cplx, lda = _mat(A, "A")
-    m, n = A.shape
+    m, ncols = A.shape
+    n = ncols if dist is None else int(n)
     dev = A.device
     if V is None:
-        V = torch.empty((n, n), dtype=A.dtype, device=dev).T.contiguous().T
+        V = torch.empty((ncols, n), dtype=A.dtype, device=dev).T
     _, ldv = _mat(V, "V")
-    sig = torch.empty(n, dtype=torch.float64, device=dev)
-    se = torch.empty(n, dtype=torch.float64, device=dev)
-    sf = torch.empty(n, dtype=torch.float64, device=dev)
-    wb = gesvj_workspace(cplx, m, n)
+    if V.shape != (n, ncols):
+        raise ValueError(f"V must be {n} x {ncols}")
+    if out is None:
+        out = dict(sigma=torch.empty(n, dtype=torch.float64, device=dev),
+                   sigma_e=torch.empty(n, dtype=torch.float64, device=dev),
+                   sigma_f=torch.empty(n, dtype=torch.float64, device=dev),
+                   perm=torch.empty(n, dtype=torch.int32, device=dev))
+    sig, se, sf, perm = out["sigma"], out["sigma_e"], out["sigma_f"], out["perm"]
+    nb = n if nblocks is None else nblocks
+    wb = gesvj_workspace(cplx, m, n, nb, dist)
     if work is None or work.numel() < wb:
         work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
-    sw = _i32(0)
+    sw, sc = _i32(0), _i32(0)
     tps = (_i64 * max(max_sweeps, 1))()
     st = lib().jsvd_gesvj(C64 if cplx else R64, m, n, _p(A), lda, _p(V), ldv, _p(sig), _p(se),
-                          _p(sf), n if nblocks is None else nblocks, max_sweeps, ct.byref(sw),
-                          ct.cast(tps, _vp), _p(work), work.numel(), _stream(stream))
+                          _p(sf), _p(perm), nb, max_sweeps, ct.byref(sw), ct.cast(tps, _vp),
+                          ct.byref(sc), _opts(s0_adjust, max_steps), _p(work), work.numel(),
+                          ct.byref(dist) if dist is not None else None, _stream(stream))
     _check(st, "jsvd_gesvj", allow=(OK, ENOCONV))
-    return dict(U=A, V=V, sigma=sig, sigma_e=se, sigma_f=sf, sweeps=sw.value,
-                tps=[tps[k] for k in range(sw.value)], status=st)
+    return dict(U=A, V=V, sigma=sig, sigma_e=se, sigma_f=sf, perm=perm, sweeps=sw.value,
+                tps=[tps[k] for k in range(sw.value)], status=st, scale=sc.value)
 
 
 def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None, stream=None,
-                  transforms=None):
+                  transforms=None, scale=None, s0_adjust=0):
     """A: (batch, m, n) CUDA tensor whose matrices are column-major, i.e.
     A.stride() == (m*n, 1, m) (use X.transpose(1,2).contiguous().transpose(1,2)).
-    In place: A becomes U.  Returns dict(U, V, sigma, sweeps, status, transforms)
-    (transforms: int64 per matrix, the number of transformed pair-steps, only
-    when a tensor is passed)."""
+    In place: A becomes U (per matrix as gesvj: G = U Sigma' on ENOCONV).
+    Returns dict(U, V, sigma, sweeps, status, transforms, scale) (transforms:
+    int64 transformed pair-steps, scale: int32 final s -- only when a tensor
+    is passed)."""
     b, m, n = A.shape
     if A.dtype not in (torch.float64, torch.complex128) or A.stride(1) != 1 or A.stride(2) < m:
         raise ValueError("A must be float64/complex128 with column-major matrices")
@@ -510,9 +572,47 @@ def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None
                                   _p(V), V.stride(2), V.stride(0), _p(sigma), max_sweeps,
                                   _p(sweeps), _p(status),
                                   _p(transforms) if transforms is not None else None,
+                                  _p(scale) if scale is not None else None, _opts(s0_adjust),
                                   _stream(stream))
     _check(st, "jsvd_gesvj_batched")
-    return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status, transforms=transforms)
+    return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status, transforms=transforms,
+                scale=scale)
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it, every rank receives it)."""
+    buf = (ct.c_char * 128)()
+    _check(lib().jsvd_nccl_unique_id(ct.cast(buf, _vp)), "jsvd_nccl_unique_id")
+    return bytes(buf)
+
+
+def nccl_comm_init(nranks, uid, rank):
+    """An NCCL communicator on the current device, owned by the caller
+    (jsvd_nccl_comm_destroy)."""
+    c = _vp()
+    buf = (ct.c_char * 128).from_buffer_copy(uid)
+    _check(lib().jsvd_nccl_comm_init(ct.byref(c), nranks, ct.cast(buf, _vp), rank),
+           "jsvd_nccl_comm_init")
+    return c.value
+
+
+def nccl_comm_destroy(comm):
+    _check(lib().jsvd_nccl_comm_destroy(comm), "jsvd_nccl_comm_destroy")
+
+
+def dist_columns(n, nblocks, rank, nranks):
+    """Global columns of rank `rank`'s local columns (jsvd_dist_columns); host."""
+    out = (_i32 * (n // nranks))()
+    _check(lib().jsvd_dist_columns(n, nblocks, rank, nranks, ct.cast(out, _vp)), "jsvd_dist_columns")
+    return list(out)
+
+
+def dist_local_pairs(n, nblocks, rank, nranks, step):
+    """Local (p, q) column pairs of rank `rank` in step `step` (jsvd_dist_local_pairs); host."""
+    out = (_i32 * (n // nranks))()
+    _check(lib().jsvd_dist_local_pairs(n, nblocks, rank, nranks, step, ct.cast(out, _vp)),
+           "jsvd_dist_local_pairs")
+    return [(out[2 * k], out[2 * k + 1]) for k in range(n // nranks // 2)]
 
 
 def fp64_peak(iters=4096, blocks=None, stream=None):

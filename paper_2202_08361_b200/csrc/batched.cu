@@ -112,7 +112,7 @@ template <bool CPLX, int NR, bool FULL, int W, int VH = 0>
 __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
-    int64_t* transforms_out, int Fm, int Kr, double tol) {
+    int64_t* transforms_out, int32_t* scale_out, int Fm, int Kr, double tol, int s0_adjust) {
   using E = typename Elem<CPLX>::T;
   constexpr int kBT = kBNH * W, kBNW = kBT / 32, kBW = W, kGPW = 32 / W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     }
     return;
   }
-  // ---- line 1: s0 = F(m) - floor(lg M0) - 1; G1 = 2^s0 G
-  int s = Fm - ilogb_bits(sM0) - 1;
+  // ---- line 1: s0 = F(m) - floor(lg M0) - 1 (+ s0_adjust, R#40); G1 = 2^s0 G
+  int s = Fm - ilogb_bits(sM0) - 1 + s0_adjust;
   for (int k = threadIdx.x; k < mi * ni; k += kBT) {
     if constexpr (CPLX) sG[k] = make_double2(scalbn_rn(sG[k].x, s), scalbn_rn(sG[k].y, s));
     else sG[k] = scalbn_rn(sG[k], s);
@@ -409,10 +409,13 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     }
   }
   __syncthreads();
+  // converged: sigma sorted (R#24), U normalised; not converged (C = S):
+  // Alg 4.1 line 41 does not finalize -- U = G, V and Sigma' (not backscaled)
+  // in column order (R#25)
   for (int r0 = warp; r0 < ni; r0 += kBNW) {
     // output column r0 <- input column j with rank r0
-    int jsel = 0;
-    for (int j = lane; j < ni; j += 32) {
+    int jsel = converged ? 0 : r0 + 1;
+    for (int j = lane; converged && j < ni; j += 32) {
       const double ej = ce[j], fj = cf[j];
       int rank = 0;
       for (int kk = 0; kk < ni; ++kk) {
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     if (lane == 0) {
       const double e = ce[j], f = cf[j];
       const bool fin = !isinf(e);
-      const double es = fin ? e - s : e;
+      const double es = (fin && converged) ? e - s : e;
       sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
     }
   }
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   for (int r0 = warp; r0 < ni; r0 += kBNW) {
     const int j = sSel[r0];
     const double e = ce[j], f = cf[j];
-    const bool fin = !isinf(e);
+    const bool fin = !isinf(e) && converged;
     const Pow2 sc(fin ? -static_cast<int>(e) : 0);
     const Divisor d = make_divisor(f);
     E* ucol = Ag + static_cast<int64_t>(r0) * lda;
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     if (status_out) status_out[b] = converged ? JSVD_OK : JSVD_ENOCONV;
     if (sweeps_out) sweeps_out[b] = C;
     if (transforms_out) transforms_out[b] = Ttot;
+    if (scale_out) scale_out[b] = s;
   }
 }
 
@@ -493,7 +497,8 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
                                           double* A, int64_t lda, int64_t strideA, double* V,
                                           int64_t ldv, int64_t strideV, double* sigma,
                                           int32_t max_sweeps, int32_t* sweeps_done,
-                                          int32_t* status, int64_t* transforms, void* stream) {
+                                          int32_t* status, int64_t* transforms, int32_t* scale,
+                                          const jsvd_gesvj_opts* opts, void* stream) {
   const bool cplx = dt == JSVD_C64;
   if (!gesvj_batched_args_ok(dt, m, n) || batch < 0 || lda < m || ldv < n || strideA < lda * n || strideV < ldv * n || max_sweeps < 0 ||
       !A || !V || !sigma)
@@ -504,13 +509,15 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
   const size_t smem = batched_smem(cplx, m, n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int Fm = Fm_host(cplx, m), Kr = cplx ? 1020 : 1022;
+  const int adj = opts ? opts->s0_adjust : 0;
+  if ((opts && opts->max_steps) || adj < -2200 || adj > 1024 - Fm) return JSVD_EINVAL;
   const double tol = std::ldexp(std::sqrt(static_cast<double>(m)), -53);
   cudaError_t e;
   auto go = [&](auto kern, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
                                                               sigma, max_sweeps, sweeps_done, status,
-                                                              transforms, Fm, Kr, tol);
+                                                              transforms, scale, Fm, Kr, tol, adj);
   };
   // W = batched_w(m) lanes per pair; NR = rows per lane
   // 16 rows of V in shared memory when 5 CTAs per SM still fit (64 x 32 complex)
@@ -519,8 +526,8 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem16));
     kern<<<static_cast<unsigned>(batch), threads, smem16, st>>>(m, n, A, lda, strideA, V, ldv,
                                                                 strideV, sigma, max_sweeps,
-                                                                sweeps_done, status, transforms, Fm,
-                                                                Kr, tol);
+                                                                sweeps_done, status, transforms, scale,
+                                                                Fm, Kr, tol, adj);
   };
   // JSVD_BATCHED_VH=0 keeps all of V in A's storage (same results, bit for
   // bit: only where V lives changes; the GPU tests compare both)

@@ -223,7 +223,7 @@ extern "C" jsvd_status jsvd_gesvj_batched_host(jsvd_dtype dt, int64_t batch, int
                         cudaMemcpyHostToDevice, s) != cudaSuccess)
       return fail_joined(p, caller, JSVD_ECUDA);
     const jsvd_status st = jsvd_gesvj_batched(dt, nb, m, n, dA, m, m * n, dV, n, n * n, ds,
-                                              max_sweeps, dsw, dst, dtr, s);
+                                              max_sweeps, dsw, dst, dtr, nullptr, nullptr, s);
     if (st != JSVD_OK) return fail_joined(p, caller, st);
     if (cudaMemcpyAsync(reinterpret_cast<char*>(U) + w * m * n * off, dA, w * m * n * nb,
                         cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -243,18 +243,21 @@ extern "C" jsvd_status jsvd_gesvj_batched_host(jsvd_dtype dt, int64_t batch, int
 
 // ---- the full SVD on host buffers: upload, jsvd_gesvj, download ------------
 namespace {
-size_t gesvj_host_parts(bool cplx, int64_t m, int64_t n, size_t* ws) {
+jsvd_status gesvj_host_parts(bool cplx, int64_t m, int64_t n, int32_t nblocks, size_t* own,
+                             size_t* ws) {
   const size_t w = cplx ? 16 : 8;
-  jsvd_gesvj_workspace(cplx ? JSVD_C64 : JSVD_R64, m, n, ws);
-  return align256(w * m * n) + align256(w * n * n) + align256(8 * n);
+  const jsvd_status st = jsvd_gesvj_workspace(cplx ? JSVD_C64 : JSVD_R64, m, n, nblocks, nullptr, ws);
+  *own = align256(w * m * n) + align256(w * n * n) + align256(8 * n);
+  return st;
 }
 }  // namespace
 
 extern "C" jsvd_status jsvd_gesvj_host_workspace(jsvd_dtype dt, int64_t m, int64_t n,
-                                                 size_t* bytes) {
+                                                 int32_t nblocks, size_t* bytes) {
   if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || n < 1 || !bytes) return JSVD_EINVAL;
-  size_t ws = 0;
-  const size_t own = gesvj_host_parts(dt == JSVD_C64, m, n, &ws);
+  size_t ws = 0, own = 0;
+  const jsvd_status st = gesvj_host_parts(dt == JSVD_C64, m, n, nblocks, &own, &ws);
+  if (st != JSVD_OK) return st;
   *bytes = own + ws;
   return JSVD_OK;
 }
@@ -262,15 +265,16 @@ extern "C" jsvd_status jsvd_gesvj_host_workspace(jsvd_dtype dt, int64_t m, int64
 extern "C" jsvd_status jsvd_gesvj_host(jsvd_dtype dt, int64_t m, int64_t n, const double* A,
                                        int64_t lda, double* U, double* V, double* sigma,
                                        int32_t nblocks, int32_t max_sweeps, int32_t* sweeps_done,
-                                       int64_t* transforms_per_sweep, void* work,
+                                       int64_t* transforms_per_sweep, int32_t* scale, void* work,
                                        size_t work_bytes, void* stream) {
   if ((dt != JSVD_R64 && dt != JSVD_C64) || m < 1 || n < 1 || lda < m || !A || !U || !V ||
       !sigma || !work)
     return JSVD_EINVAL;
   const bool cplx = dt == JSVD_C64;
   const size_t w = cplx ? 16 : 8;
-  size_t ws = 0;
-  const size_t own = gesvj_host_parts(cplx, m, n, &ws);
+  size_t ws = 0, own = 0;
+  const jsvd_status q = gesvj_host_parts(cplx, m, n, nblocks, &own, &ws);
+  if (q != JSVD_OK) return q;
   if (work_bytes < own + ws) return JSVD_ENOMEM;
   char* base = static_cast<char*>(work);
   double* dA = reinterpret_cast<double*>(base);
@@ -280,9 +284,9 @@ extern "C" jsvd_status jsvd_gesvj_host(jsvd_dtype dt, int64_t m, int64_t n, cons
   // A (ld = lda on the host) -> packed m x n on the device
   if (cudaMemcpy2DAsync(dA, w * m, A, w * lda, w * m, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return JSVD_ECUDA;
-  const jsvd_status s = jsvd_gesvj(dt, m, n, dA, m, dV, n, ds, nullptr, nullptr, nblocks,
-                                   max_sweeps, sweeps_done, transforms_per_sweep, base + own, ws,
-                                   stream);
+  const jsvd_status s = jsvd_gesvj(dt, m, n, dA, m, dV, n, ds, nullptr, nullptr, nullptr, nblocks,
+                                   max_sweeps, sweeps_done, transforms_per_sweep, scale, nullptr,
+                                   base + own, ws, nullptr, stream);
   if (s != JSVD_OK && s != JSVD_ENOCONV) return s;
   if (cudaMemcpyAsync(U, dA, w * m * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaMemcpyAsync(V, dV, w * n * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

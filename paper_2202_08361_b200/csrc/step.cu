@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   if (P.pairs) {
     p = P.pairs[2 * pair];
     q = P.pairs[2 * pair + 1];
+  } else if (P.dist_nr > 0) {
+    dist_pair(static_cast<int>(P.n), static_cast<int>(P.B), P.dist_nr, P.dist_rank,
+              static_cast<int>(P.step), static_cast<int>(pair), p, q);
   } else {
     strategy_pair(P.n, P.B, P.step, pair, p, q);
   }

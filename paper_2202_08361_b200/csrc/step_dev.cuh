@@ -521,4 +521,56 @@ __device__ __host__ __forceinline__ void strategy_pair(int64_t n64, int64_t B64,
   q = x < y ? y : x;
 }
 
+// ---- the block round-robin sharded over nr ranks ----------
+// Rank g owns the per = B/2/nr position pairs (i, B-1-i), i in [g per,
+// (g+1) per): local slot 2k holds position g per + k, slot 2k+1 position
+// B-1-(g per + k); slot s is local columns [s b, (s+1) b).  In round r
+// position k holds block circle_player(B, r, k) (round 0: block k).
+__device__ __host__ __forceinline__ int dist_slot_position(int B, int nr, int rank, int slot) {
+  const int i = rank * (B / 2 / nr) + slot / 2;
+  return (slot & 1) ? B - 1 - i : i;
+}
+
+// (rank, slot) holding circle position pos
+__device__ __host__ __forceinline__ void dist_owner(int B, int nr, int pos, int& rank, int& slot) {
+  const int per = B / 2 / nr;
+  const bool low = pos < B / 2;
+  const int i = low ? pos : B - 1 - pos;
+  rank = i / per;
+  slot = 2 * (i - rank * per) + (low ? 0 : 1);
+}
+
+// global column of local column l at round 0 (every sweep starts and ends
+// there: B - 1 rounds move every block once around the circle)
+__device__ __host__ __forceinline__ int dist_gcol(int n, int B, int nr, int rank, int l) {
+  const int b = n / B;
+  return dist_slot_position(B, nr, rank, l / b) * b + l % b;
+}
+
+// pair l (of n/(2 nr)) of step `step` on rank `rank`, as LOCAL columns (p, q)
+// ordered as the global pair of strategy_pair (p the lower global column):
+// phase I is flat RR inside every local block; in phase II the block pair of
+// slots (2k, 2k+1) is (circle_player(B, r, i), circle_player(B, r, B-1-i)),
+// i = rank per + k, and step t of the round pairs column j of the lower
+// block with column (j + t) mod b of the higher.
+__device__ __host__ __forceinline__ void dist_pair(int n, int B, int nr, int rank, int step, int l,
+                                                   int& p, int& q) {
+  const int b = n / B;
+  if (step < b - 1) {
+    const int slot = l / (b / 2), i = l - slot * (b / 2);
+    const int x = circle_player(b, step, i), y = circle_player(b, step, b - 1 - i);
+    p = slot * b + (x < y ? x : y);
+    q = slot * b + (x < y ? y : x);
+    return;
+  }
+  const int s2 = step - (b - 1), rr = s2 / b, tt = s2 - rr * b;
+  const int k = l / b, j = l - k * b;
+  const int i = rank * (B / 2 / nr) + k;
+  const int u = circle_player(B, rr, i), v = circle_player(B, rr, B - 1 - i);
+  const int lo = u < v ? 2 * k : 2 * k + 1, hi = u < v ? 2 * k + 1 : 2 * k;
+  const int jt = j + tt;
+  p = lo * b + j;
+  q = hi * b + (jt >= b ? jt - b : jt);
+}
+
 }  // namespace jsvd

@@ -12,6 +12,7 @@ struct StepParams {
   int64_t ldv;
   const int32_t* pairs;  // explicit pairs, or nullptr -> strategy (B, step)
   int64_t B, step;
+  int dist_nr, dist_rank;  // dist_nr > 0: this rank's local pairs of the sharded ordering
   double tol;
   double* col_e;
   double* col_f;

@@ -1,7 +1,19 @@
-"""The column-block-sharded SVD with the library's kernels on one GPU: P = 1,
-2, 4, 8 virtual ranks (LocalRanks: device copies for the block exchange; the
-ranks run one after another, no kernel waits on another).  Results must be
-bitwise identical for every P, to jsvd_gesvj(nblocks=16) and to the oracle."""
+"""The column-block-sharded jsvd_gesvj (a jsvd_dist: the schedule, block
+exchange and collectives inside libjsvd) on one GPU:
+ - P = 1, 2, 4, 8 thread ranks (dist.ThreadGroup: host-staged transport; each
+   rank's kernels on its own stream, only the host rendezvous synchronises --
+   no kernel waits on another rank's kernel);
+ - a world of one NCCL rank (NcclDist.single) with JSVD_DIST_SELF_P2P: every
+   block move goes through ncclSend/ncclRecv to self inside ncclGroupStart/End,
+   M-tilde and T through ncclAllReduce, the sort keys through ncclAllGather;
+ - two processes on the GPU with the CUDA kernels and a gloo (CPU-staged)
+   transport.
+Results must be bitwise identical for every P and transport, to
+jsvd_gesvj(nblocks=16) on one GPU and to the oracle -- converged, capped
+ and with the Eq. (skr) rescale firing (R#40)."""
+import os
+import socket
+
 import numpy as np
 import pytest
 import torch
@@ -16,32 +28,142 @@ def _bits(a):
     return (a.view(np.float64) if np.iscomplexobj(a) else a).view(np.uint64)
 
 
-@pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("m,n", [(64, 32), (300, 64), (2049, 96)])
-def test_dist_virtual_ranks_bitwise(cplx, m, n):
-    import paper_2202_08361_b200 as J
-    from paper_2202_08361_b200.dist import (BlockSchedule, CudaCompute, LocalRanks,
-                                            gather_columns, gesvj_dist, scatter_columns)
-    rng = np.random.default_rng(m + n + cplx)
+def _case(cplx, m, n, seed=0):
+    rng = np.random.default_rng(m + n + cplx + seed)
     A = rng.standard_normal((m, n)) * 2.0 ** rng.integers(-20, 20, n)
     if cplx:
         A = A + 1j * rng.standard_normal((m, n))
-    R = O.RSpec.make(*J.step_rspec(cplx, m))
-    ref = O.gesvj(A, R, B=16, max_sweeps=30)
+    return A
+
+
+def _rspec(cplx, m):
+    # R#15 for m <= 2048 (complex) / 4096 (real): one CTA of W = 256 lanes
+    W = 256 if (m <= 2048 or (not cplx and m <= 4096)) else 512
+    offs = [16, 8, 4, 2, 1, 128, 64, 32] + ([256] if W == 512 else [])
+    return O.RSpec.make(W, 1, offs)
+
+
+def _assemble(outs, cols, n, status):
+    U = np.zeros((outs[0]["U"].shape[0], n), dtype=outs[0]["U"].cpu().numpy().dtype)
+    V = np.zeros((n, n), dtype=U.dtype)
+    for o, c in zip(outs, cols):
+        U[:, c] = o["U"].T.contiguous().cpu().numpy().T
+        V[:, c] = o["V"].T.contiguous().cpu().numpy().T
+    perm = outs[0]["perm"].cpu().numpy()
+    if status == 0:
+        U, V = U[:, perm], V[:, perm]
+    return U, V, perm
+
+
+def _check(ref, outs, cols, n):
+    for o in outs:
+        assert o["status"] == ref["status"] and o["sweeps"] == ref["sweeps"]
+        assert list(o["tps"]) == list(ref["tps"]) and o["scale"] == ref["scale"]
+        for k in ("sigma", "sigma_e", "sigma_f"):
+            assert np.array_equal(_bits(o[k].cpu().numpy()), _bits(ref[k])), k
+    U, V, perm = _assemble(outs, cols, n, ref["status"])
+    if ref["status"] != 0:
+        assert np.array_equal(perm, np.arange(n))
+    assert np.array_equal(_bits(U), _bits(ref["U"]))
+    assert np.array_equal(_bits(V), _bits(ref["V"]))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("m,n", [(64, 32), (300, 64), (2049, 96)])
+def test_dist_thread_ranks_bitwise(cplx, m, n):
+    import paper_2202_08361_b200 as J
+    from paper_2202_08361_b200.dist import run_thread_ranks
+    A = _case(cplx, m, n)
+    assert J.step_rspec(cplx, m)[:2] == (_rspec(cplx, m).W, 1)
+    ref = O.gesvj(A, _rspec(cplx, m), B=16, max_sweeps=30)
     g = torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T
     lib = J.gesvj(g, nblocks=16, max_sweeps=30)
     assert np.array_equal(_bits(lib["U"].T.contiguous().cpu().numpy().T), _bits(ref["U"]))
-    dt = torch.complex128 if cplx else torch.float64
     for P in (1, 2, 4, 8):
-        S = BlockSchedule(n, 16, P)
-        Gts = [torch.from_numpy(np.ascontiguousarray(A[:, scatter_columns(None, S, r)].T))
-               .to(dt).cuda() for r in range(P)]
-        res = gesvj_dist(Gts, S, LocalRanks(P), CudaCompute(), cplx=cplx)
-        assert res["sweeps"] == ref["sweeps"] and list(res["tps"]) == list(ref["tps"])
-        U = np.array(gather_columns([G.cpu().numpy() for G in res["Gts"]], S)).T
-        V = np.array(gather_columns([V.cpu().numpy() for V in res["Vts"]], S)).T
-        perm = res["perm"]
-        assert np.array_equal(_bits(U[:, perm]), _bits(ref["U"])), P
-        assert np.array_equal(_bits(V[:, perm]), _bits(ref["V"])), P
-        assert np.array_equal(_bits(res["sigma"]), _bits(ref["sigma"]))
-        assert np.array_equal(_bits(res["sigma_e"]), _bits(ref["sigma_e"]))
+        outs, cols = run_thread_ranks(A, 16, P, max_sweeps=30)
+        _check(ref, outs, cols, n)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_dist_thread_ranks_capped_and_rescaled(cplx):
+    from paper_2202_08361_b200.dist import run_thread_ranks
+    m, n = 96, 64
+    A = _case(cplx, m, n, seed=3)
+    K = 1020 if cplx else 1022
+    for kw in (dict(max_sweeps=2), dict(max_sweeps=30, s0_adjust=K + 1 - O.Fm(cplx, m))):
+        ref = O.gesvj(A, _rspec(cplx, m), B=16, **kw)
+        for P in (2, 8):
+            outs, cols = run_thread_ranks(A, 16, P, **kw)
+            _check(ref, outs, cols, n)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_dist_nccl_world_one_self_p2p(cplx):
+    # the NCCL transport executed on one GPU: ncclSend/ncclRecv to self for
+    # every block move, ncclAllReduce, ncclAllGather
+    import paper_2202_08361_b200 as J
+    from paper_2202_08361_b200.dist import NcclDist, gesvj_sharded, local_columns
+    m, n = 300, 64
+    A = _case(cplx, m, n, seed=5)
+    ref = O.gesvj(A, _rspec(cplx, m), B=16, max_sweeps=30)
+    nd = NcclDist.single(flags=J.DIST_SELF_P2P)
+    try:
+        cols = local_columns(n, 16, 0, 1)
+        part = torch.from_numpy(np.ascontiguousarray(A[:, cols].T)).cuda().T
+        out = gesvj_sharded(part, n, 16, nd.dist, max_sweeps=30)
+        torch.cuda.synchronize()
+        _check(ref, [out], [cols], n)
+        # and without SELF_P2P (local moves as device copies)
+        nd.dist.flags = 0
+        part = torch.from_numpy(np.ascontiguousarray(A[:, cols].T)).cuda().T
+        out = gesvj_sharded(part, n, 16, nd.dist, max_sweeps=30)
+        torch.cuda.synchronize()
+        _check(ref, [out], [cols], n)
+    finally:
+        nd.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cplx, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_08361_b200.dist import GlooTransport, gesvj_sharded, local_columns
+        m, n = 300, 64
+        A = _case(cplx, m, n, seed=7)
+        tr = GlooTransport()
+        cols = local_columns(n, 16, rank, world)
+        part = torch.from_numpy(np.ascontiguousarray(A[:, cols].T)).cuda().T
+        out = gesvj_sharded(part, n, 16, tr.dist, max_sweeps=30)
+        torch.cuda.synchronize()
+        q.put((rank, {k: (v.cpu() if torch.is_tensor(v) else v) for k, v in out.items()}, cols))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_dist_two_processes_gloo_staged(cplx):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cplx, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    m, n = 300, 64
+    A = _case(cplx, m, n, seed=7)
+    ref = O.gesvj(A, _rspec(cplx, m), B=16, max_sweeps=30)
+    _check(ref, [g[1] for g in got], [g[2] for g in got], n)

@@ -1,7 +1,8 @@
 """GPU parity of the Jacobi-SVD entry points against the oracle, BITWISE:
 jsvd_strategy_pairs, jsvd_sweep_step (every kernel geometry: single CTA and
 2/4/8-CTA clusters), jsvd_gesvj (U, V, sigma, (e,f), sweeps, T per sweep).
-The oracle is given the reduction spec R the library reports for (dtype, m)."""
+The oracle is given the reduction spec R of DESIGN.md R#15 for (dtype, m),
+written out here (and checked against what the library reports)."""
 import numpy as np
 import pytest
 import torch
@@ -19,9 +20,31 @@ def J():
     return J
 
 
+# The step kernel's reduction spec R (R#15), written out per
+# (dtype, m) rather than queried from the library under test: W = 256 CL lanes
+# (CL CTAs of 256 threads), element i on lane i mod W, lanes combined by xor
+# offsets 16..1 (warp), 128, 64, 32 (warps of the CTA), then W/2 .. 256 (the
+# CTAs of the cluster).  W is the smallest power of two >= 256 with W * NR >= m
+# (NR = 16 real / 8 complex rows per lane in registers); beyond W = 2048 the
+# kernel holds 2 NR rows per lane (half in shared memory), so W * 2 NR >= m.
+_W_TABLE = {
+    (False, 1): 256, (False, 7): 256, (False, 64): 256, (False, 255): 256, (False, 256): 256,
+    (False, 257): 256, (False, 300): 256, (False, 1000): 256, (False, 2049): 256,
+    (False, 4096): 256, (False, 8191): 512, (False, 16384): 1024, (False, 20001): 2048,
+    (False, 65536): 2048,
+    (True, 1): 256, (True, 7): 256, (True, 64): 256, (True, 255): 256, (True, 256): 256,
+    (True, 257): 256, (True, 300): 256, (True, 1000): 256, (True, 2048): 256, (True, 2049): 512,
+    (True, 4096): 512, (True, 8191): 1024, (True, 16384): 2048, (True, 20001): 2048,
+    (True, 32768): 2048,
+}
+_W_TABLE.update({(c, m): 256 for c in (False, True) for m in (2, 4, 6, 8, 16, 40, 100, 512, 600)})
+
+
 def rspec(J, cplx, m):
-    W, c, offs = J.step_rspec(cplx, m)
-    return O.RSpec.make(W, c, offs)
+    W = _W_TABLE[(cplx, m)]
+    offs = [16, 8, 4, 2, 1, 128, 64, 32] + [W >> k for k in range(1, 16) if (W >> k) >= 256]
+    assert J.step_rspec(cplx, m) == (W, 1, tuple(offs)), (cplx, m)  # the library agrees
+    return O.RSpec.make(W, 1, offs)
 
 
 def colmajor_gpu(A):
@@ -128,20 +151,62 @@ def test_gesvj_bitwise(J, cplx, m, n, B):
     assert bits_equal(out["sigma_f"].cpu().numpy(), ref["sigma_f"])
 
 
-def test_gesvj_capped_run_and_errors(J):
-    rng = np.random.default_rng(5)
-    A = rng.standard_normal((64, 16))
-    R = rspec(J, False, 64)
-    ref = O.gesvj(A, R, max_sweeps=2)
-    out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), max_sweeps=2)
-    assert out["status"] == ref["status"] == 1  # ENOCONV (R#25)
-    assert bits_equal(to_np(out["U"]), ref["U"])
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("max_sweeps", [0, 1, 2])
+def test_gesvj_capped_run_is_G_and_sigma_prime(J, cplx, max_sweeps):
+    # Alg 4.1 line 41 (R#25): C = S -> no finalize; A holds
+    # G = U Sigma' (scaled by 2^s), sigma Sigma' in column order, perm identity
+    rng = np.random.default_rng(5 + cplx)
+    A = rng.standard_normal((64, 16)) + (1j * rng.standard_normal((64, 16)) if cplx else 0)
+    R = rspec(J, cplx, 64)
+    ref = O.gesvj(A, R, max_sweeps=max_sweeps)
+    out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), max_sweeps=max_sweeps)
+    assert out["status"] == ref["status"] == 1  # ENOCONV
+    assert out["sweeps"] == ref["sweeps"] == max_sweeps and out["scale"] == ref["scale"]
+    assert list(out["tps"]) == list(ref["tps"])
+    for k in ("U", "V"):
+        assert bits_equal(to_np(out[k]), ref[k]), k
+    for k in ("sigma", "sigma_e", "sigma_f"):
+        assert bits_equal(out[k].cpu().numpy(), ref[k]), k
+    assert np.array_equal(out["perm"].cpu().numpy(), np.arange(16))
+
+
+def test_gesvj_errors(J):
     with pytest.raises(J.JsvdError):
         J.gesvj(colmajor_gpu(np.zeros((8, 4))))
     bad = np.ones((8, 4))
     bad[2, 2] = np.nan
     with pytest.raises(J.JsvdError):
         J.gesvj(colmajor_gpu(bad))
+    with pytest.raises(J.JsvdError):  # s0_adjust that would overflow G1 (R#40)
+        J.gesvj(colmajor_gpu(np.ones((8, 4))), s0_adjust=1024 - O.Fm(False, 8) + 1)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("adj_from_K", [0, 1, 2])
+def test_gesvj_rescale_fires_bitwise(J, cplx, adj_from_K):
+    # R#40: s0_adjust = K + 1 - F(m) + d starts at floor(lg M~1) = K + d, so
+    # the Eq. (skr) check fires at step 0 (d >= 1) or in mid-run when a
+    # component reaches 2^(K+1) (d = 0) -- the M-tilde "track" shortcut
+    # (pairs with max(e) > K - 1 tracked) is exercised right at the boundary.
+    K = 1020 if cplx else 1022
+    rng = np.random.default_rng(70 + cplx + 3 * adj_from_K)
+    fired = 0
+    for m, n in ((2, 2), (4, 4), (6, 4), (8, 8), (40, 24)):
+        A = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cplx else 0)
+        adj = K + 1 - O.Fm(cplx, m) + adj_from_K
+        R = O.RSpec.make(256, 1, [16, 8, 4, 2, 1, 128, 64, 32])  # R#15 for m <= 2048
+        assert J.step_rspec(cplx, m) == (256, 1, (16, 8, 4, 2, 1, 128, 64, 32))
+        ref = O.gesvj(A, R, max_sweeps=40, s0_adjust=adj)
+        out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), max_sweeps=40, s0_adjust=adj)
+        assert out["status"] == ref["status"] and out["sweeps"] == ref["sweeps"]
+        assert out["scale"] == ref["scale"], (m, n)
+        assert bits_equal(to_np(out["U"]), ref["U"]) and bits_equal(to_np(out["V"]), ref["V"])
+        for k in ("sigma", "sigma_e", "sigma_f"):
+            assert bits_equal(out[k].cpu().numpy(), ref[k]), k
+        base = O.gesvj(A, R, max_sweeps=40)
+        fired += ref["scale"] < base["scale"] + adj
+    assert fired >= 2
 
 
 def test_config3_full_size_step_bitwise(J):
@@ -258,3 +323,90 @@ def test_gesvj_batched_v_placement_is_invisible(J, monkeypatch, cplx):
         if a.is_complex():
             a, c = torch.view_as_real(a), torch.view_as_real(c)
         assert torch.equal(a, c), k
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gesvj_batched_rescale_and_cap_bitwise(J, cplx):
+    # the batched kernel's own rescale (every step, flat RR) and its line-41
+    # branch: s0_adjust = K + 1 - F(m) (fires in mid-run, R#40), and a 2-sweep
+    # cap (ENOCONV: G = U Sigma', Sigma' unsorted, R#25); scale per matrix
+    K = 1020 if cplx else 1022
+    rng = np.random.default_rng(123 + cplx)
+    for m, n in ((64, 32), (16, 16), (40, 24)):
+        b = 9
+        A = rng.standard_normal((b, m, n)) + (1j * rng.standard_normal((b, m, n)) if cplx else 0)
+        W, c, offs = J.batched_rspec(cplx, m)
+        assert (W, c, offs) == (8, 1, (4, 2, 1))  # R#15: 8 lanes per pair for m <= 64
+        R = O.RSpec.make(8, 1, [4, 2, 1])
+        for kw in (dict(s0_adjust=K + 1 - O.Fm(cplx, m)), dict(max_sweeps=2)):
+            ref = O.gesvj_batched(A, R, **{"max_sweeps": 40, **kw})
+            g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+            sc = torch.empty(b, dtype=torch.int32, device="cuda")
+            out = J.gesvj_batched(g, scale=sc, **{"max_sweeps": 40, **kw})
+            torch.cuda.synchronize()
+            assert np.array_equal(out["status"].cpu().numpy(), ref["status"]), kw
+            assert np.array_equal(out["sweeps"].cpu().numpy(), ref["sweeps"]), kw
+            assert np.array_equal(sc.cpu().numpy(), ref["scale"]), kw
+            U = out["U"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+            V = out["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+            assert bits_equal(U, ref["U"]) and bits_equal(V, ref["V"]), kw
+            assert bits_equal(out["sigma"].cpu().numpy(), ref["sigma"]), kw
+
+
+# ------------------------------------------- the paths configs[4] takes (R#15)
+@pytest.mark.parametrize("cplx,m,nv", [(True, 32768, 8192), (True, 16384, 8192),
+                                       (True, 2048, 1024), (True, 2048, 1030),
+                                       (False, 4096, 1024), (False, 65536, 8192),
+                                       (True, 300, 1500)])
+def test_sweep_step_long_V_bitwise(J, cplx, m, nv):
+    # Alg 3.4 applied to V with l = n rows: V has nv rows (the
+    # order of the whole SVD) while the step holds 8 columns (4 pairs), as a
+    # column-block rank does.  nv > 2 W reaches the V rows of cluster ranks
+    # >= 1 and the strided tail loop of the step kernel; complex m <= 2048 is
+    # the single-CTA (W = 256) geometry with a tail beyond row 512.
+    ncols = 8
+    rng = np.random.default_rng(m + nv + cplx)
+    A = _scaled_input(rng, m, ncols, cplx, specials=False)
+    V = rng.standard_normal((nv, ncols)) + (1j * rng.standard_normal((nv, ncols)) if cplx else 0)
+    V = np.asfortranarray(V)
+    R = rspec(J, cplx, m)
+    G_ref, V_ref = A.copy(order="F"), V.copy(order="F")
+    g, v = colmajor_gpu(A), colmajor_gpu(V)
+    for k in range(2):
+        pairs = np.array([[0, 5], [1, 7], [2, 4], [3, 6]] if k == 0 else [[0, 1], [2, 3], [4, 5], [6, 7]],
+                         np.int32)
+        ref = O.step(G_ref, V_ref, pairs, R)
+        out = J.sweep_step(g, v, torch.from_numpy(pairs).cuda())
+        torch.cuda.synchronize()
+        assert int(out["t"].item()) == ref["t"] == 4
+        assert bits_equal(to_np(g), G_ref), k
+        assert bits_equal(to_np(v), V_ref), k
+        assert out["mmax"].item() == ref["mmax"]
+
+
+def test_config5_full_size_step_sampled_bitwise(J):
+    # BASELINE configs[4] at full size (complex 32768 x 8192, 4.3 GB) in the
+    # bench's launch configuration: one step of all 4096 pairs (block RR,
+    # B = 16) of the scaled matrix with V = I of order 8192; the oracle
+    # recomputes 6 sampled pairs from their columns before the step.
+    m, n = 32768, 8192
+    g, _ = synth.svd_cfg5_torch(m, n, device="cuda")  # (m, n) column-major complex128
+    mx = torch.view_as_real(g).abs().max().item()
+    s0 = O.Fm(True, m) - int(np.floor(np.log2(mx))) - 1
+    torch.view_as_real(g).mul_(2.0 ** s0)  # exact power-of-two scaling (no subnormals here)
+    v = torch.eye(n, dtype=torch.complex128, device="cuda").T.contiguous().T
+    step = 600  # a phase-II step of the block ordering
+    pairs = J.strategy_pairs(n, 16, step)
+    sample = np.random.default_rng(1).choice(n // 2, 6, replace=False)
+    pl = pairs.cpu().numpy()[sample]
+    cols = pl.reshape(-1)
+    G0 = np.asfortranarray(g[:, cols].cpu().numpy())
+    V0 = np.asfortranarray(v[:, cols].cpu().numpy())
+    out = J.sweep_step(g, v, pairs)
+    torch.cuda.synchronize()
+    local = np.arange(12, dtype=np.int32).reshape(6, 2)
+    ref = O.step(G0, V0, local, rspec(J, True, m))
+    assert bits_equal(g[:, cols].cpu().numpy(), G0)
+    assert bits_equal(v[:, cols].cpu().numpy(), V0)
+    ce, cf = out["col_e"].cpu().numpy(), out["col_f"].cpu().numpy()
+    assert bits_equal(ce[cols], ref["col_e"]) and bits_equal(cf[cols], ref["col_f"])
