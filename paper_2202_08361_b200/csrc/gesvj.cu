@@ -18,8 +18,10 @@
 //            Sigma' are returned as they are (R#25).
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "jsvd_host.h"
@@ -513,9 +515,13 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
   double* Galt = dist ? reinterpret_cast<double*>(ws + WL.g2) : nullptr;
   double* Valt = dist ? reinterpret_cast<double*>(ws + WL.v2) : nullptr;
   const bool self_p2p = dist && dist->nccl_comm && (dist->flags & JSVD_DIST_SELF_P2P);
+  // Point-to-point operations between two ranks match in the order they are
+  // posted, so both sides list them by the SOURCE circle position (G then V
+  // per block): a rank sending several blocks to one peer -- only itself,
+  // with JSVD_DIST_SELF_P2P -- then pairs every send with its receive.
   auto exchange = [&]() -> jsvd_status {
     const int nslots = static_cast<int>(nl / b);
-    std::vector<Comm::Op> ops;
+    std::vector<std::pair<int, Comm::Op>> sends, recvs;
     for (int sl = 0; sl < nslots; ++sl) {  // outgoing
       const int pos = dist_slot_position(nblocks, nr, dist->rank, sl);
       const int dpos = pos == 0 ? 0 : (pos >= 2 ? pos - 1 : nblocks - 1);
@@ -529,8 +535,8 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
         CK(cudaMemcpyAsync(reinterpret_cast<char*>(Valt) + ds * vblk, vs, vblk,
                            cudaMemcpyDeviceToDevice, st));
       } else {
-        ops.push_back({dr, 0, gs, gblk});
-        ops.push_back({dr, 0, vs, vblk});
+        sends.push_back({2 * pos, {dr, 0, gs, gblk}});
+        sends.push_back({2 * pos + 1, {dr, 0, vs, vblk}});
       }
     }
     for (int ds = 0; ds < nslots; ++ds) {  // incoming
@@ -539,9 +545,17 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
       int sr, ss;
       dist_owner(nblocks, nr, spos, sr, ss);
       if (sr == dist->rank && !self_p2p) continue;
-      ops.push_back({sr, 1, reinterpret_cast<char*>(Galt) + ds * gblk, gblk});
-      ops.push_back({sr, 1, reinterpret_cast<char*>(Valt) + ds * vblk, vblk});
+      recvs.push_back({2 * spos, {sr, 1, reinterpret_cast<char*>(Galt) + ds * gblk, gblk}});
+      recvs.push_back({2 * spos + 1, {sr, 1, reinterpret_cast<char*>(Valt) + ds * vblk, vblk}});
     }
+    const auto by_pos = [](const std::pair<int, Comm::Op>& a, const std::pair<int, Comm::Op>& b) {
+      return a.first < b.first;
+    };
+    std::sort(sends.begin(), sends.end(), by_pos);
+    std::sort(recvs.begin(), recvs.end(), by_pos);
+    std::vector<Comm::Op> ops;
+    for (const auto& o : sends) ops.push_back(o.second);
+    for (const auto& o : recvs) ops.push_back(o.second);
     CS(comm.p2p(ops));
     std::swap(Gcur, Galt);
     std::swap(Vcur, Valt);

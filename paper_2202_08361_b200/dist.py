@@ -136,7 +136,7 @@ class GlooTransport(_HostTransport):
 
     def sendrecv(self, ops):
         # the k-th operation to / from one peer matches the peer's k-th (the
-        # library lists each block's G then V, blocks in slot order)
+        # library lists both sides by source circle position, G then V)
         seq, reqs = {}, []
         for peer, dirn, a in ops:
             tag = seq.get((peer, dirn), 0)

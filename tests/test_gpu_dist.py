@@ -43,13 +43,20 @@ def _rspec(cplx, m):
     return O.RSpec.make(W, 1, offs)
 
 
+def _np(x):
+    """numpy copy of a (column-major view of a) tensor, or x itself"""
+    if torch.is_tensor(x):
+        return x.T.contiguous().cpu().numpy().T if x.dim() == 2 else x.cpu().numpy()
+    return x
+
+
 def _assemble(outs, cols, n, status):
-    U = np.zeros((outs[0]["U"].shape[0], n), dtype=outs[0]["U"].cpu().numpy().dtype)
+    U = np.zeros((_np(outs[0]["U"]).shape[0], n), dtype=_np(outs[0]["U"]).dtype)
     V = np.zeros((n, n), dtype=U.dtype)
     for o, c in zip(outs, cols):
-        U[:, c] = o["U"].T.contiguous().cpu().numpy().T
-        V[:, c] = o["V"].T.contiguous().cpu().numpy().T
-    perm = outs[0]["perm"].cpu().numpy()
+        U[:, c] = _np(o["U"])
+        V[:, c] = _np(o["V"])
+    perm = _np(outs[0]["perm"])
     if status == 0:
         U, V = U[:, perm], V[:, perm]
     return U, V, perm
@@ -60,7 +67,7 @@ def _check(ref, outs, cols, n):
         assert o["status"] == ref["status"] and o["sweeps"] == ref["sweeps"]
         assert list(o["tps"]) == list(ref["tps"]) and o["scale"] == ref["scale"]
         for k in ("sigma", "sigma_e", "sigma_f"):
-            assert np.array_equal(_bits(o[k].cpu().numpy()), _bits(ref[k])), k
+            assert np.array_equal(_bits(_np(o[k])), _bits(ref[k])), k
     U, V, perm = _assemble(outs, cols, n, ref["status"])
     if ref["status"] != 0:
         assert np.array_equal(perm, np.arange(n))
@@ -145,7 +152,8 @@ def _worker(rank, world, port, cplx, q):
         part = torch.from_numpy(np.ascontiguousarray(A[:, cols].T)).cuda().T
         out = gesvj_sharded(part, n, 16, tr.dist, max_sweeps=30)
         torch.cuda.synchronize()
-        q.put((rank, {k: (v.cpu() if torch.is_tensor(v) else v) for k, v in out.items()}, cols))
+        # numpy, not tensors: the queue must not hold fds of this process's storage
+        q.put((rank, {k: _np(v) for k, v in out.items()}, cols))
     finally:
         dist.destroy_process_group()
 
