@@ -902,6 +902,14 @@ def run_jsvd(args):
         extra["all_converged"] = bool((wl.st == 0).all().item())
         extra["hbm_roofline_frac"] = achieved / peak
         extra["transformed_pair_steps_per_matrix"] = float(wl.tr.double().mean().item())
+        # the paper's Fig 5.4 breakdown for this kernel (jsvd_batched_phase_profile,
+        # a clock64-instrumented build of the same kernel, run after the timing)
+        wl.prepare()
+        pr = J.batched_phase_profile(wl.A.transpose(1, 2), stream=stream)
+        torch.cuda.synchronize()
+        extra["phase_breakdown"] = {
+            who: {k: round(v / max(d["sweep loop"], 1), 4) for k, v in d.items() if k != "sweep loop"}
+            for who, d in pr.items()}
         # FP64-pipe-bound kernel: algorithmic FP64 operations per second vs the
         # measured DFMA throughput of jsvd_fp64_peak
         ops = wl.fp64_ops()

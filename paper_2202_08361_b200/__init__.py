@@ -97,6 +97,9 @@ def lib():
         L.jsvd_gesvj_batched.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64,
                                          _i64, _vp, _i32, _vp, _vp, _vp, _vp,
                                          ct.POINTER(GesvjOpts), _vp]
+        L.jsvd_batched_phase_profile.restype = ct.c_int
+        L.jsvd_batched_phase_profile.argtypes = [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp,
+                                                 _i64, _i64, _vp, _i32, _vp, _vp]
         L.jsvd_nccl_unique_id.restype = ct.c_int
         L.jsvd_nccl_unique_id.argtypes = [_vp]
         L.jsvd_nccl_comm_init.restype = ct.c_int
@@ -577,6 +580,27 @@ def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None
     _check(st, "jsvd_gesvj_batched")
     return dict(U=A, V=V, sigma=sigma, sweeps=sweeps, status=status, transforms=transforms,
                 scale=scale)
+
+
+PHASES = ("A: norms + dot", "wait after A", "B: test, Gram, EVD (warp 0) / V rotation (others)",
+          "wait after B", "C: G rotation", "wait after C", "rescale check", "sweep loop")
+
+
+def batched_phase_profile(A, max_sweeps=30, stream=None):
+    """jsvd_batched_phase_profile on (batch, 64, n) column-major matrices (in
+    place, as gesvj_batched): per-phase cycles of warp 0 and of the other
+    warps, summed over the CTAs -- dict(warp0={phase: cycles}, others=...)."""
+    b, m, n = A.shape
+    cplx = A.dtype == torch.complex128
+    V = torch.empty((b, n, n), dtype=A.dtype, device=A.device).transpose(1, 2)
+    sig = torch.empty((b, n), dtype=torch.float64, device=A.device)
+    prof = torch.zeros(16, dtype=torch.int64, device=A.device)
+    _check(lib().jsvd_batched_phase_profile(C64 if cplx else R64, b, m, n, _p(A), A.stride(2),
+                                            A.stride(0), _p(V), V.stride(2), V.stride(0), _p(sig),
+                                            max_sweeps, _p(prof), _stream(stream)),
+           "jsvd_batched_phase_profile")
+    p = prof.cpu().tolist()
+    return dict(warp0=dict(zip(PHASES, p[:8])), others=dict(zip(PHASES, p[8:])))
 
 
 def nccl_unique_id():

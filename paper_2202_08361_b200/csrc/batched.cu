@@ -108,11 +108,16 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
 }
 
 // FULL: m == W NR (configs[3]: 64 = 8 x 8), so no row needs a bounds check
-template <bool CPLX, int NR, bool FULL, int W, int VH = 0>
+// PROF (diagnostic, jsvd_batched_phase_profile): every warp accumulates the
+// clock64 cycles it spends in each phase of a step and in each barrier wait,
+// added into prof[(warp == 0 ? 0 : 1) * 8 + k] at exit -- the paper's
+// breakdown of Fig 5.4 for this kernel.
+template <bool CPLX, int NR, bool FULL, int W, int VH = 0, bool PROF = false>
 __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
-    int64_t* transforms_out, int32_t* scale_out, int Fm, int Kr, double tol, int s0_adjust) {
+    int64_t* transforms_out, int32_t* scale_out, int Fm, int Kr, double tol, int s0_adjust,
+    unsigned long long* prof = nullptr) {
   using E = typename Elem<CPLX>::T;
   constexpr int kBT = kBNH * W, kBNW = kBT / 32, kBW = W, kGPW = 32 / W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -231,10 +236,24 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   int C = 0;
   int64_t Ttot = 0;  // transformed pair-steps (thread 0)
   bool converged = false;
+  // PROF: cycles per warp in [0] phase A, [1] wait after A, [2] phase B
+  // (warp 0) / V rotation (warps 1..), [3] wait after B, [4] phase C, [5] wait
+  // after C, [6] rescale check, [7] whole sweep loop
+  unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = 0, tloop = 0;
+  const auto mark = [&](int k) {
+    if constexpr (PROF) {
+      const long long t = clock64();
+      pc[k] += static_cast<unsigned long long>(t - tprev);
+      tprev = t;
+    }
+  };
+  if constexpr (PROF) tloop = tprev = clock64();
   for (C = 0; C < max_sweeps; ++C) {
     if (threadIdx.x == 0) sT = 0;
     for (int k = 0; k < ni - 1; ++k, ++gstep) {
       PairSlot* slots = slots2 + (gstep & 1) * np;
+      if constexpr (PROF) tprev = clock64();
       // ---- line 6: rescale check (every step for flat round-robin); M-tilde
       // is normal here (G is scaled to ~ omega / m), so its high word's
       // exponent field is floor(lg M-tilde)
@@ -252,6 +271,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
           __syncthreads();
         }
       }
+      mark(6);
       // ---- phase A: lane group per pair: exponent max, SSQ, prescaled dot
       for (int l0 = 0; l0 < np; l0 += kBNH) {  // uniform trip count: both halves shuffle
         const int l = l0 + hw;
@@ -292,7 +312,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
           sl.eq = eq;
         }
       }
+      mark(0);
       __syncthreads();
+      mark(1);
       // ---- phase B: norms' f, the dot's division, convergence test,
       // Grammian and EVD of the step, one lane per pair
       if (warp == 0) {
@@ -329,7 +351,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       } else if (pend_k >= 0) {  // the lane groups of warps 1..: V of the previous step
         rotate_v(slots2 + pend_buf * np, pend_k, hw - kGPW, kBNH - kGPW, hl, kBW);
       }
+      mark(2);
       __syncthreads();
+      mark(3);
       // ---- phase C: rotations of G (Alg 3.4), M-tilde
       uint32_t Mw = 0;
       for (int l = hw; l < np; l += kBNH) {
@@ -363,7 +387,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       pend_buf = gstep & 1;
       Mw = __reduce_max_sync(0xffffffffu, Mw);
       if (lane == 0 && Mw > sMt) atomicMax(&sMt, Mw);
+      mark(4);
       __syncthreads();
+      mark(5);
     }
     if (threadIdx.x == 0) Ttot += sT;
     if (sT == 0) {
@@ -372,6 +398,11 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       break;
     }
     __syncthreads();
+  }
+  if constexpr (PROF) {
+    pc[7] = static_cast<unsigned long long>(clock64() - tloop);
+    if (lane == 0)
+      for (int k = 0; k < 8; ++k) atomicAdd(&prof[(warp == 0 ? 0 : 1) * 8 + k], pc[k]);
   }
   if (pend_k >= 0) {  // the last step's V rotation
     rotate_v(slots2 + pend_buf * np, pend_k, hw, kBNH, hl, kBW);
@@ -493,12 +524,12 @@ bool gesvj_batched_args_ok(jsvd_dtype dt, int64_t m, int64_t n) {
 
 using namespace jsvd;
 
-extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t m, int64_t n,
-                                          double* A, int64_t lda, int64_t strideA, double* V,
-                                          int64_t ldv, int64_t strideV, double* sigma,
-                                          int32_t max_sweeps, int32_t* sweeps_done,
-                                          int32_t* status, int64_t* transforms, int32_t* scale,
-                                          const jsvd_gesvj_opts* opts, void* stream) {
+static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t n, double* A,
+                                int64_t lda, int64_t strideA, double* V, int64_t ldv,
+                                int64_t strideV, double* sigma, int32_t max_sweeps,
+                                int32_t* sweeps_done, int32_t* status, int64_t* transforms,
+                                int32_t* scale, const jsvd_gesvj_opts* opts, void* stream,
+                                unsigned long long* prof) {
   const bool cplx = dt == JSVD_C64;
   if (!gesvj_batched_args_ok(dt, m, n) || batch < 0 || lda < m || ldv < n || strideA < lda * n || strideV < ldv * n || max_sweeps < 0 ||
       !A || !V || !sigma)
@@ -517,7 +548,8 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
                                                               sigma, max_sweeps, sweeps_done, status,
-                                                              transforms, scale, Fm, Kr, tol, adj);
+                                                              transforms, scale, Fm, Kr, tol, adj,
+                                                              prof);
   };
   // W = batched_w(m) lanes per pair; NR = rows per lane
   // 16 rows of V in shared memory when 5 CTAs per SM still fit (64 x 32 complex)
@@ -527,7 +559,7 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
     kern<<<static_cast<unsigned>(batch), threads, smem16, st>>>(m, n, A, lda, strideA, V, ldv,
                                                                 strideV, sigma, max_sweeps,
                                                                 sweeps_done, status, transforms, scale,
-                                                                Fm, Kr, tol, adj);
+                                                                Fm, Kr, tol, adj, prof);
   };
   // JSVD_BATCHED_VH=0 keeps all of V in A's storage (same results, bit for
   // bit: only where V lives changes; the GPU tests compare both)
@@ -541,9 +573,11 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
     cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
     vh16 = 5 * (smem16 + 320 + static_cast<size_t>(reserved)) <= static_cast<size_t>(per_sm);
   }
+  if (prof && !(m == 64 && vh16)) return JSVD_EINVAL;  // the profile covers configs[3]'s kernel
   auto pick = [&](auto cplx_t) {
     constexpr bool C = decltype(cplx_t)::value;
-    if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true>, 128);
+    else if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
     else if (m == 64 && vh16) go16(batched_svd_kernel<C, 8, true, 8, 16>, 128);
     else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
     else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);
@@ -556,6 +590,30 @@ extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t 
   note_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
+}
+
+extern "C" jsvd_status jsvd_gesvj_batched(jsvd_dtype dt, int64_t batch, int64_t m, int64_t n,
+                                          double* A, int64_t lda, int64_t strideA, double* V,
+                                          int64_t ldv, int64_t strideV, double* sigma,
+                                          int32_t max_sweeps, int32_t* sweeps_done,
+                                          int32_t* status, int64_t* transforms, int32_t* scale,
+                                          const jsvd_gesvj_opts* opts, void* stream) {
+  return batched_impl(dt, batch, m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps,
+                      sweeps_done, status, transforms, scale, opts, stream, nullptr);
+}
+
+extern "C" jsvd_status jsvd_batched_phase_profile(jsvd_dtype dt, int64_t batch, int64_t m,
+                                                  int64_t n, double* A, int64_t lda,
+                                                  int64_t strideA, double* V, int64_t ldv,
+                                                  int64_t strideV, double* sigma,
+                                                  int32_t max_sweeps, unsigned long long* prof,
+                                                  void* stream) {
+  if (!prof) return JSVD_EINVAL;
+  if (cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream)) !=
+      cudaSuccess)
+    return JSVD_ECUDA;
+  return batched_impl(dt, batch, m, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps,
+                      nullptr, nullptr, nullptr, nullptr, nullptr, stream, prof);
 }
 
 extern "C" jsvd_status jsvd_batched_rspec(jsvd_dtype dt, int64_t m, int32_t* W, int32_t* c,

@@ -1,13 +1,10 @@
 #!/bin/bash
-# usage: scripts/gpu_check.sh TAG [ncu-kernel-regex] -- GPU tests + bench (+ optional ncu full capture)
-TAG=${1:-run}; KRE=${2:-}
-OUT=gpurun_out/$TAG; mkdir -p $OUT
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
-if [ -n "$KRE" ]; then
-  timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_short.json 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KRE -s 5 -c 1 \
-     -o $OUT/prof python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $OUT/ncu_full.log 2>&1
-fi
+# usage: scripts/gpu_check.sh TAG [WORKLOADS...] -- GPU tests + smoke + bench lines (no ncu)
+TAG=$1; shift; OUT=gpurun_out/$TAG; mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/smi.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q -rf --timeout 900 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+for w in "$@"; do
+  timeout 1200 python bench.py --workload $w --no-cpu-baseline > $OUT/bench_$w.json 2> $OUT/bench_$w.err; echo "rc=$?" >> $OUT/bench_$w.err
+done
 echo done
