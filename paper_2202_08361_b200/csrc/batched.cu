@@ -31,6 +31,19 @@
 
 namespace jsvd {
 
+// Fast mode: every value of G~ is 0 or has |x| >= 2^-400,
+// i.e. a high word (sign masked) of at least kFastLo.  lo_hi_min folds
+// hi(|x|) - 1 into a running minimum: 0 maps to 0xffffffff and passes;
+// nonzero values below 2^-1022 cannot occur in fast mode (their rotation
+// inputs are >= 2^-400, so every nonzero output is >= 2^-905).
+constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;
+__device__ __forceinline__ uint32_t lo_hi_min(double x, uint32_t m) {
+  return min(m, abs_hi(x) - 1u);
+}
+__device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
+  return min(m, min(abs_hi(x.x) - 1u, abs_hi(x.y) - 1u));
+}
+
 // W lanes per pair (R.W = 8 for m <= 64, 16 above) and 16 lane groups per CTA
 // (16 W threads): one pass of phases A and C covers the 16 pairs of n = 32
 constexpr int kBNH = 16;
@@ -112,7 +125,7 @@ __device__ __forceinline__ void eg_from_ssq(int E, double ssq, int& e, double& g
 // clock64 cycles it spends in each phase of a step and in each barrier wait,
 // added into prof[(warp == 0 ? 0 : 1) * 8 + k] at exit -- the paper's
 // breakdown of Fig 5.4 for this kernel.
-template <bool CPLX, int NR, bool FULL, int W, int VH = 0, bool PROF = false>
+template <bool CPLX, int NR, bool FULL, int W, int VH = 0, bool PROF = false, bool FAST = true>
 __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     int64_t m, int64_t n, double* A, int64_t lda, int64_t strideA, double* Vg, int64_t ldv,
     int64_t strideV, double* sigma, int max_sweeps, int32_t* sweeps_out, int32_t* status_out,
@@ -136,6 +149,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   __shared__ unsigned long long sM0;
   __shared__ uint32_t sMt;  // high word of M-tilde (its floor(lg) is all Eq. skr uses)
   __shared__ int sT;
+  __shared__ int sBad;  // fast mode: the invariant of DESIGN.md 4.6 failed this step
   __shared__ uint64_t wred[kBNW];
   __shared__ int sSel[64];  // finalize: input column of each output rank
 
@@ -154,8 +168,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     sPairs[2 * k + 1] = static_cast<uint8_t>(q);
   }
 
-  // ---- load A, M0 = max |component| (NaN -> inf), V = I
-  uint64_t mx = 0;
+  // ---- load A, M0 = max |component| (NaN -> inf), V = I; mn = the smallest
+  // nonzero |component| (bits; zero -> all ones), for the fast mode's check
+  uint64_t mx = 0, mn = ~0ull;
   for (int k = threadIdx.x; k < mi * ni; k += kBT) {
     const int j = k / mi, i = k - j * mi;
     const E x = Ag[static_cast<int64_t>(j) * lda + i];
@@ -163,13 +178,20 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     if constexpr (CPLX) {
       mx = max(mx, abs_bits(fmin(fabs(x.x), static_cast<double>(INFINITY))));
       mx = max(mx, abs_bits(fmin(fabs(x.y), static_cast<double>(INFINITY))));
+      if (FAST) mn = min(mn, min(abs_bits(x.x) - 1, abs_bits(x.y) - 1));
     } else {
       mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
+      if (FAST) mn = min(mn, abs_bits(x) - 1);
     }
   }
   {
     const uint64_t M0 = cta_max_u64<kBT>(mx, wred);
     if (threadIdx.x == 0) sM0 = M0;
+    __syncthreads();
+  }
+  uint64_t mn_all = 0;
+  if constexpr (FAST) {
+    mn_all = ~cta_max_u64<kBT>(~mn, wred);  // min over the CTA
     __syncthreads();
   }
   const double M0 = __longlong_as_double(static_cast<long long>(sM0));
@@ -181,13 +203,39 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     }
     return;
   }
-  // ---- line 1: s0 = F(m) - floor(lg M0) - 1 (+ s0_adjust, R#40); G1 = 2^s0 G
+  // ---- line 1: s0 = F(m) - floor(lg M0) - 1 (+ s0_adjust, R#40); G1 = 2^s0 G.
+  // Fast mode: shared memory holds G~ = G 2^-cs with cs =
+  // floor(lg M~1), i.e. G~ = A 2^-floor(lg M0), when every nonzero |a_ij| is
+  // at least 2^-400 M0 (then every value of G~ is 0 or in [2^-400, 2^16]).
   int s = Fm - ilogb_bits(sM0) - 1 + s0_adjust;
-  for (int k = threadIdx.x; k < mi * ni; k += kBT) {
-    if constexpr (CPLX) sG[k] = make_double2(scalbn_rn(sG[k].x, s), scalbn_rn(sG[k].y, s));
-    else sG[k] = scalbn_rn(sG[k], s);
+  bool fast = false;
+  int cs = 0;
+  if constexpr (FAST) {
+    const int lm0 = ilogb_bits(sM0);
+    fast = (mn_all == ~0ull || ilogb_bits(mn_all + 1) >= lm0 - 400) && lm0 + s <= 1023;
+    cs = lm0 + s;
   }
-  if (threadIdx.x == 0) sMt = hi32(scalbn_rn(M0, s));
+  {
+    const int sh = fast ? s - cs : s;
+    for (int k = threadIdx.x; k < mi * ni; k += kBT) {
+      if constexpr (CPLX) sG[k] = make_double2(scalbn_rn(sG[k].x, sh), scalbn_rn(sG[k].y, sh));
+      else sG[k] = scalbn_rn(sG[k], sh);
+    }
+  }
+  if (threadIdx.x == 0) {
+    sMt = hi32(scalbn_rn(M0, s));
+    sBad = 0;
+  }
+  // leave the fast mode (CTA-uniform, after a barrier): G = G~ 2^cs exactly,
+  // every value of G~ being 0 or normal
+  const auto leave_fast = [&]() {
+    for (int kk = threadIdx.x; kk < mi * ni; kk += kBT) {
+      if constexpr (CPLX) sG[kk] = make_double2(scalbn_rn(sG[kk].x, cs), scalbn_rn(sG[kk].y, cs));
+      else sG[kk] = scalbn_rn(sG[kk], cs);
+    }
+    fast = false;
+    __syncthreads();
+  };
   // V = I over A's storage (every read of A above precedes the barrier in
   // cta_max_u64)
   for (int k = threadIdx.x; k < ni * ni; k += kBT) {
@@ -260,7 +308,13 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       {
         const int lm = static_cast<int>(sMt >> 20) - 1023;
         const int sn = (Kr - lm < 0) ? Fm - lm - 1 : 0;
-        if (sn != 0) {  // uniform
+        if (sn != 0 && fast) {  // G = G~ 2^cs: the scaling moves into cs
+          __syncthreads();
+          if (threadIdx.x == 0) sMt = hi32(scalbn_rn(mkd(sMt, 0u), sn));
+          cs += sn;
+          s += sn;
+          __syncthreads();
+        } else if (sn != 0) {  // uniform
           __syncthreads();
           for (int kk = threadIdx.x; kk < mi * ni; kk += kBT) {
             if constexpr (CPLX) sG[kk] = make_double2(scalbn_rn(sG[kk].x, sn), scalbn_rn(sG[kk].y, sn));
@@ -272,7 +326,41 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
         }
       }
       mark(6);
-      // ---- phase A: lane group per pair: exponent max, SSQ, prescaled dot
+      // ---- phase A: lane group per pair: exponent max, SSQ, prescaled dot.
+      // Fast mode: G~ needs no prescaling -- the SSQ and the dot of the raw
+      // values are exact power-of-two multiples of the oracle's (DESIGN.md
+      // 4.6), accumulated in one pass in the same lane order R; B rescales.
+      if (fast) {
+        for (int l0 = 0; l0 < np; l0 += kBNH) {
+          const int l = l0 + hw;
+          const bool act = l < np;
+          const int p = act ? sPairs[2 * (k * np + l)] : 0;
+          const int q = act ? sPairs[2 * (k * np + l) + 1] : 1;
+          const E* gp = sG + p * mi;
+          const E* gq = sG + q * mi;
+          double sp = 0.0, sq = 0.0, ar = 0.0, ai = 0.0;
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const int i = j * kBW + hl;
+            const E xpj = (FULL || i < mi) ? gp[i] : Elem<CPLX>::zero();
+            const E xqj = (FULL || i < mi) ? gq[i] : Elem<CPLX>::zero();
+            sp = ssq_acc(xpj, sp);
+            sq = ssq_acc(xqj, sq);
+            dot_acc(xqj, xpj, ar, ai);
+          }
+          sp = hsum<W>(sp);
+          sq = hsum<W>(sq);
+          ar = hsum<W>(ar);
+          if (CPLX) ai = hsum<W>(ai);
+          if (act && hl == 0) {
+            PairSlot& sl = slots[l];
+            sl.ar = ar;
+            sl.ai = ai;
+            sl.gp = sp;  // the raw SSQ of G~ (B derives (e, f))
+            sl.gq = sq;
+          }
+        }
+      } else
       for (int l0 = 0; l0 < np; l0 += kBNH) {  // uniform trip count: both halves shuffle
         const int l = l0 + hw;
         const bool act = l < np;
@@ -323,14 +411,43 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
           const int l = l0 + lane;
           const bool act = l < np;
           const PairSlot& s0 = slots[act ? l : 0];
-          const bool zp = s0.ep == kIntMin, zq = s0.eq == kIntMin;
-          const double fp = zp ? 1.0 : sqrt_plain(s0.gp), fq = zq ? 1.0 : sqrt_plain(s0.gq);
-          const double ep = zp ? -INFINITY : static_cast<double>(s0.ep);
-          const double eq = zq ? -INFINITY : static_cast<double>(s0.eq);
+          bool zp, zq;
+          int iep, ieq;
+          double gpv, gqv, arv = s0.ar, aiv = s0.ai;
+          if (fast) {
+            // the raw SSQ of G~ = G 2^-cs is 2^(2E - 2cs) times the oracle's
+            // SSQ of x 2^-E (exactly), so R#14's (e, f) follow with E := cs;
+            // the dot of G~ is 2^(e_q + e_p - 2cs) times the prescaled one
+            zp = !(s0.gp > 0.0);
+            zq = !(s0.gq > 0.0);
+            iep = ieq = kIntMin;
+            gpv = gqv = 1.0;
+            if (!zp) eg_from_ssq(cs, s0.gp, iep, gpv);
+            if (!zq) eg_from_ssq(cs, s0.gq, ieq, gqv);
+            if (!(zp || zq)) {
+              const double f2 = pow2i(2 * cs - iep - ieq);
+              arv *= f2;
+              aiv *= f2;
+            }
+            if (act) {
+              slots[l].ep = iep;
+              slots[l].eq = ieq;
+            }
+          } else {
+            zp = s0.ep == kIntMin;
+            zq = s0.eq == kIntMin;
+            iep = s0.ep;
+            ieq = s0.eq;
+            gpv = s0.gp;
+            gqv = s0.gq;
+          }
+          const double fp = zp ? 1.0 : sqrt_plain(gpv), fq = zq ? 1.0 : sqrt_plain(gqv);
+          const double ep = zp ? -INFINITY : static_cast<double>(iep);
+          const double eq = zq ? -INFINITY : static_cast<double>(ieq);
           // z = (ar, ai) / fl(fq fp), fl(fq fp) in [1, 4) (Alg 3.1 line 8)
           const Rcp d = rcp_plain(fq * fp);
-          const double zr = dot_div(s0.ar, d, kFull);
-          const double zi = CPLX ? dot_div(s0.ai, d, kFull) : 0.0;
+          const double zr = dot_div(arv, d, kFull);
+          const double zi = CPLX ? dot_div(aiv, d, kFull) : 0.0;
           const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
           const bool tr = act && !(zp || zq) && tol <= az;  // Alg 3.2
           if (__any_sync(kFull, tr)) {
@@ -343,6 +460,10 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
               slots[l].C = o.sr;
               slots[l].S = o.si;
             }
+            // fast mode needs C, S in {0} u [2^-400, 1]
+            const bool bad = fast && tr &&
+                             (abs_hi(o.sr) - 1u < kFastLo - 1u || abs_hi(o.si) - 1u < kFastLo - 1u);
+            if (__any_sync(kFull, bad) && lane == 0) sBad = 1;
           }
           if (act) slots[l].transform = tr;
           tcount += __popc(__ballot_sync(0xffffffffu, tr));
@@ -354,8 +475,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
       mark(2);
       __syncthreads();
       mark(3);
+      if (fast && sBad) leave_fast();  // a C or S below 2^-400: rotate in G's scale
       // ---- phase C: rotations of G (Alg 3.4), M-tilde
-      uint32_t Mw = 0;
+      uint32_t Mw = 0, lmin = ~0u;
       for (int l = hw; l < np; l += kBNH) {
         const PairSlot& sl = slots[l];
         if (!sl.transform) continue;
@@ -380,16 +502,21 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
               Mw = hi_max(a, Mw);
               Mw = hi_max(bq, Mw);
             }
+            if (fast) lmin = lo_hi_min(a, lo_hi_min(bq, lmin));
           }
         }
       }
       pend_k = k;
       pend_buf = gstep & 1;
       Mw = __reduce_max_sync(0xffffffffu, Mw);
+      if (fast && Mw) Mw += static_cast<uint32_t>(cs) << 20;  // G = G~ 2^cs (normal values)
       if (lane == 0 && Mw > sMt) atomicMax(&sMt, Mw);
+      // fast mode keeps every value of G~ in {0} u [2^-400, 2^16]
+      if (fast && lmin < kFastLo - 1u) sBad = 1;
       mark(4);
       __syncthreads();
       mark(5);
+      if (fast && sBad) leave_fast();
     }
     if (threadIdx.x == 0) Ttot += sT;
     if (sT == 0) {
@@ -408,6 +535,7 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
     rotate_v(slots2 + pend_buf * np, pend_k, hw, kBNH, hl, kBW);
     __syncthreads();
   }
+  if (fast) leave_fast();
   // ---- finalize: norms with the step's R (R#23),
   // U = G diag(2^-e / f), sigma, sort
   for (int j0 = 0; j0 < ni; j0 += kBNH) {  // lane group per column, uniform trip count
@@ -574,10 +702,16 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
     vh16 = 5 * (smem16 + 320 + static_cast<size_t>(reserved)) <= static_cast<size_t>(per_sm);
   }
   if (prof && !(m == 64 && vh16)) return JSVD_EINVAL;  // the profile covers configs[3]'s kernel
+  // JSVD_BATCHED_FAST=0: never enter the scaled fast mode (same
+  // results bit for bit -- the GPU tests compare both)
+  const char* fast_s = getenv("JSVD_BATCHED_FAST");
+  const bool fast_env = !fast_s || atoi(fast_s) != 0;
   auto pick = [&](auto cplx_t) {
     constexpr bool C = decltype(cplx_t)::value;
-    if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true>, 128);
+    if (prof && fast_env) go16(batched_svd_kernel<C, 8, true, 8, 16, true>, 128);
+    else if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true, false>, 128);
     else if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    else if (m == 64 && vh16 && !fast_env) go16(batched_svd_kernel<C, 8, true, 8, 16, false, false>, 128);
     else if (m == 64 && vh16) go16(batched_svd_kernel<C, 8, true, 8, 16>, 128);
     else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
     else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);

@@ -412,3 +412,48 @@ def test_config5_full_size_step_sampled_bitwise(J):
     assert bits_equal(v[:, cols].cpu().numpy(), V0)
     ce, cf = out["col_e"].cpu().numpy(), out["col_f"].cpu().numpy()
     assert bits_equal(ce[cols], ref["col_e"]) and bits_equal(cf[cols], ref["col_f"])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("kind", ["gauss", "graded", "tiny_entries", "zeros", "rank_def", "rescale"])
+def test_gesvj_batched_fast_mode_is_invisible(J, monkeypatch, cplx, kind):
+    # the batched kernel keeps G~ = G 2^-cs in shared memory
+    # while every value is 0 or in [2^-400, 2^16]; the fast and the exact mode
+    # (JSVD_BATCHED_FAST=0) give the same bits, and both equal the oracle --
+    # including inputs that start outside the fast mode, leave it in mid-run
+    # (cancellation to tiny values, tiny C / S), or rescale (R#40).
+    rng = np.random.default_rng(55 + cplx)
+    b, m, n = 24, 64, 32
+    A = rng.standard_normal((b, m, n)) + (1j * rng.standard_normal((b, m, n)) if cplx else 0)
+    adj = 0
+    if kind == "graded":
+        A = A * 2.0 ** rng.integers(-180, 180, (b, 1, n))
+    elif kind == "tiny_entries":
+        A[:, ::7, ::5] *= 2.0 ** -450          # beyond the fast range from the start
+        A[::3, 5, 9] = 5e-324                   # subnormal entries
+    elif kind == "zeros":
+        A[:, 3, :] = 0.0
+        A[::2, :, 4] = 0.0
+    elif kind == "rank_def":
+        A[:, :, 7] = A[:, :, 3] * 2.0 ** 9     # parallel columns: cancellation to ~0
+        A[:, :, 11] = A[:, :, 2] + 2.0 ** -420 * A[:, :, 5]
+    elif kind == "rescale":
+        adj = (1021 if cplx else 1023) - O.Fm(cplx, m)
+    R = O.RSpec.make(8, 1, [4, 2, 1])
+    ref = O.gesvj_batched(A, R, max_sweeps=40, s0_adjust=adj)
+    outs = []
+    for fast in ("1", "0"):
+        monkeypatch.setenv("JSVD_BATCHED_FAST", fast)
+        g = torch.from_numpy(np.ascontiguousarray(np.transpose(A, (0, 2, 1)))).cuda().transpose(1, 2)
+        sc = torch.empty(b, dtype=torch.int32, device="cuda")
+        o = J.gesvj_batched(g, max_sweeps=40, scale=sc, s0_adjust=adj)
+        torch.cuda.synchronize()
+        outs.append(o)
+        assert np.array_equal(o["status"].cpu().numpy(), ref["status"]), fast
+        assert np.array_equal(o["sweeps"].cpu().numpy(), ref["sweeps"]), fast
+        assert np.array_equal(sc.cpu().numpy(), ref["scale"]), fast
+        ok = [k for k in range(b) if ref["status"][k] >= 0]
+        U = o["U"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+        V = o["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
+        assert bits_equal(U[ok], ref["U"][ok]) and bits_equal(V[ok], ref["V"][ok]), fast
+        assert bits_equal(o["sigma"].cpu().numpy()[ok], ref["sigma"][ok]), fast
