@@ -212,8 +212,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   int cs = 0;
   if constexpr (FAST) {
     const int lm0 = ilogb_bits(sM0);
-    fast = (mn_all == ~0ull || ilogb_bits(mn_all + 1) >= lm0 - 400) && lm0 + s <= 1023;
     cs = lm0 + s;
+    // G = G~ 2^cs must stay normal (G~ >= 2^-905 for cs >= 0) and finite
+    fast = (mn_all == ~0ull || ilogb_bits(mn_all + 1) >= lm0 - 400) && cs >= 0 && cs <= 1000;
   }
   {
     const int sh = fast ? s - cs : s;
