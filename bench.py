@@ -1155,7 +1155,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         args.steps = {"evd_c64": 200, "evd_r64": 200, "evd_c32": 200, "step_r64": 300, "gesvj_r64": 2,
-                      "batched_c64": 3, "step_c64": 50, "dist_c64": 100, "norm_c64": 50,
+                      "batched_c64": 3, "step_c64": 50, "dist_c64": 3, "norm_c64": 50,
                       "gs_r64": 50}[args.workload]
     if args.impl == "reference":
         run_reference(args)
