@@ -583,7 +583,8 @@ def gesvj_batched(A, max_sweeps=30, V=None, sigma=None, sweeps=None, status=None
 
 
 PHASES = ("A: norms + dot", "wait after A", "B: test, Gram, EVD (warp 0) / V rotation (others)",
-          "wait after B", "C: G rotation", "wait after C", "rescale check", "sweep loop")
+          "wait after B", "C: G rotation", "wait after C", "rescale check, loads, line 41",
+          "sweep loop")
 
 
 def batched_phase_profile(A, max_sweeps=30, stream=None):

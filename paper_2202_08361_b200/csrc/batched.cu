@@ -730,12 +730,13 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
     if (e != cudaSuccess) return JSVD_ECUDA;
     marked = 1;
     prof = nullptr;
-  } else if (prof) {
+  } else if (prof && !(m == 64 && vh16)) {
     return JSVD_EINVAL;  // the profile covers configs[3]'s kernels
   }
   auto pick = [&](auto cplx_t) {
     constexpr bool C = decltype(cplx_t)::value;
-    if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true, false>, 128);
+    else if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
     else if (m == 64 && vh16) go16(batched_svd_kernel<C, 8, true, 8, 16, false, false>, 128);
     else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
     else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);

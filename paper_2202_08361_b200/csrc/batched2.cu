@@ -51,17 +51,6 @@ struct Pair {
   int transform, pad;
 };
 
-struct Slot {
-  long long b;       // matrix index (-1: idle, no more work)
-  long long Ttot;    // transformed pair-steps
-  int k, C, T;       // step, sweep, transformations this sweep
-  int s, cs;         // scaling exponent of G (oracle) and of G~ = G 2^-cs
-  uint32_t Mt;       // high word of M-tilde (G's scale)
-  int bad;           // the fast domain was left this tick
-  int pend;          // step whose V rotation is pending (-1: none)
-  int fin;           // 1 converged, 2 capped: finalize after this tick
-};
-
 __device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
   return min(m, min(abs_hi(x.x) - 1u, abs_hi(x.y) - 1u));
 }
@@ -105,7 +94,6 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   Pair* sP = reinterpret_cast<Pair*>(sG0 + 2 * kM * n);      // [2 slot][2 buf][16]
   double* sE = reinterpret_cast<double*>(sP + 2 * 2 * kGroups);  // [2][2][32] finalize (e, f)
   uint8_t* sPairs = reinterpret_cast<uint8_t*>(sE + 2 * 2 * 32);  // (n-1) x np pivot pairs
-  __shared__ Slot sl[2];
   __shared__ uint64_t wred[4];
   __shared__ int sSel[32];
 
@@ -132,24 +120,48 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   };
   if constexpr (PROF) tprev = clock64();
 
-  // ---- load matrix b into slot s (all threads); returns with the slot either
-  // running (fast domain), or idle for this b (ERANK / ENONFINITE written, or
-  // abandoned to the exact kernel) -- the caller then loads the next one
+  // Per-slot state, uniform over the CTA: every thread keeps its own copy in
+  // registers and updates it identically (no shared-memory round trips on
+  // the per-step path).  Shared: the cumulative transformation count (added
+  // by phase B), the domain flag (set by B and C) and M-tilde (max-reduced
+  // by C).
+  long long rb[2] = {-1, -1};  // matrix (-1: no more work)
+  int rk[2] = {0, 0}, rC[2] = {0, 0}, rs[2] = {0, 0}, rcs[2] = {0, 0};
+  int rpend[2] = {-1, -1}, rfin[2] = {0, 0}, rT0[2] = {0, 0};
+  __shared__ int sTc[2], sBad[2];
+  __shared__ uint32_t sMt[2];
+
+  // ---- load matrix b into slot s (all threads); true: the slot runs it (fast
+  // domain); false: ERANK / ENONFINITE written, or handed to batched.cu's kernel
   const auto load = [&](int s, long long b) -> bool {
     const E* Ag = reinterpret_cast<const E*>(A) + b * strideA;
     E* sG = G_of(s);
     uint64_t mx = 0, mn = ~0ull;
-    for (int k = threadIdx.x; k < kM * n; k += kT) {
-      const int j = k / kM, i = k - j * kM;
-      const E x = Ag[static_cast<int64_t>(j) * lda + i];
-      sG[k] = x;
-      if constexpr (CPLX) {
-        mx = max(mx, abs_bits(fmin(fabs(x.x), static_cast<double>(INFINITY))));
-        mx = max(mx, abs_bits(fmin(fabs(x.y), static_cast<double>(INFINITY))));
-        mn = min(mn, min(abs_bits(x.x) - 1, abs_bits(x.y) - 1));
-      } else {
-        mx = max(mx, abs_bits(fmin(fabs(x), static_cast<double>(INFINITY))));
-        mn = min(mn, abs_bits(x) - 1);
+    constexpr int kPer = 8;  // elements per thread and round (loads issued together)
+    for (int k0 = 0; k0 < kM * n; k0 += kT * kPer) {
+      E x[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int k = k0 + u * kT + threadIdx.x;
+        if (k < kM * n) {
+          const int j = k / kM, i = k - j * kM;
+          x[u] = Ag[static_cast<int64_t>(j) * lda + i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int k = k0 + u * kT + threadIdx.x;
+        if (k < kM * n) {
+          sG[k] = x[u];
+          if constexpr (CPLX) {
+            mx = max(mx, abs_bits(fmin(fabs(x[u].x), static_cast<double>(INFINITY))));
+            mx = max(mx, abs_bits(fmin(fabs(x[u].y), static_cast<double>(INFINITY))));
+            mn = min(mn, min(abs_bits(x[u].x) - 1, abs_bits(x[u].y) - 1));
+          } else {
+            mx = max(mx, abs_bits(fmin(fabs(x[u]), static_cast<double>(INFINITY))));
+            mn = min(mn, abs_bits(x[u]) - 1);
+          }
+        }
       }
     }
     const uint64_t M0b = cta_max_u64<kT>(mx, wred);
@@ -188,17 +200,17 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       else v = i == j ? 1.0 : 0.0;
       Vb[static_cast<int64_t>(j) * ldv + i] = v;
     }
+    rb[s] = b;
+    rk[s] = rC[s] = 0;
+    rs[s] = s0;
+    rcs[s] = cs;
+    rpend[s] = -1;
+    rfin[s] = max_sweeps == 0 ? 2 : 0;
+    rT0[s] = 0;
     if (threadIdx.x == 0) {
-      Slot& S = sl[s];
-      S.b = b;
-      S.Ttot = 0;
-      S.k = S.C = S.T = 0;
-      S.s = s0;
-      S.cs = cs;
-      S.Mt = hi32(scalbn_rn(M0, s0));
-      S.bad = 0;
-      S.pend = -1;
-      S.fin = max_sweeps == 0 ? 2 : 0;
+      sMt[s] = hi32(scalbn_rn(M0, s0));
+      sBad[s] = 0;
+      sTc[s] = 0;
     }
     __syncthreads();
     return true;
@@ -210,14 +222,13 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       if (load(s, b)) return;
       b += nslots_total;
     }
-    if (threadIdx.x == 0) sl[s].b = -1;
-    __syncthreads();
+    rb[s] = -1;
   };
 
   // V rotation of slot s's step kk with the pair parameters in buffer buf:
-  // the pairs [l0, np) step ls, lanes lane0 / lanes of the caller's group
+  // the pairs [l0, np) step ls, lanes of the caller's group
   const auto rotate_v = [&](int s, int kk, int buf, int l0, int ls) {
-    E* Vb = reinterpret_cast<E*>(Vg) + sl[s].b * strideV;
+    E* Vb = reinterpret_cast<E*>(Vg) + rb[s] * strideV;
     const Pair* P = sP + (s * 2 + buf) * kGroups;
     for (int l = l0; l < np; l += ls) {
       const Pair& pr = P[l];
@@ -250,8 +261,8 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   // ---- line 41 for slot s: converged -> norms (R#23), U = G diag(2^-e/f),
   // sigma sorted (R#24), V permuted; capped -> G = U Sigma', Sigma' (R#25)
   const auto finalize = [&](int s) {
-    const Slot S = sl[s];
-    const bool conv = S.fin == 1;
+    const bool conv = rfin[s] == 1;
+    const int cs_ = rcs[s];
     E* sG = G_of(s);
     double* ce = sE + s * 64;
     double* cf = ce + 32;
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
         int e;
         double gg;
         if (ssq > 0.0) {
-          eg_of(S.cs, ssq, e, gg);
+          eg_of(cs_, ssq, e, gg);
           ce[j] = static_cast<double>(e);
           cf[j] = sqrt_plain(gg);
         } else {
@@ -276,38 +287,39 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       }
     }
     __syncthreads();
-    const long long b = S.b;
-    E* Ag = reinterpret_cast<E*>(A) + b * strideA;
-    E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
-    for (int r0 = warp; r0 < n; r0 += kT / 32) {  // output column r0 <- column j
-      int jsel = conv ? 0 : r0 + 1;
-      for (int j = lane; conv && j < n; j += 32) {
+    // rank of every column (stable by (e desc, f desc, index asc); R#24):
+    // sSel[rank] = column
+    if (threadIdx.x < n) {
+      const int j = threadIdx.x;
+      int rank = j;
+      if (conv) {
         const double ej = ce[j], fj = cf[j];
-        int rank = 0;
+        rank = 0;
         for (int kk = 0; kk < n; ++kk) {
           const double ek = ce[kk], fk = cf[kk];
           rank += ((ek > ej) || (ek == ej && (fk > fj || (fk == fj && kk < j)))) ? 1 : 0;
         }
-        if (rank == r0) jsel = j + 1;
       }
-      jsel = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(jsel));
-      const int j = jsel - 1;
-      if (lane == 0) {
-        sSel[r0] = j;
-        const double e = ce[j], f = cf[j];
-        const bool fin = !isinf(e);
-        const double es = (fin && conv) ? e - S.s : e;
-        sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
-      }
+      sSel[rank] = j;
     }
     __syncthreads();
+    const long long b = rb[s];
+    if (threadIdx.x < n) {
+      const int r0 = threadIdx.x, j = sSel[r0];
+      const double e = ce[j], f = cf[j];
+      const bool fin = !isinf(e);
+      const double es = (fin && conv) ? e - rs[s] : e;
+      sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
+    }
+    E* Ag = reinterpret_cast<E*>(A) + b * strideA;
+    E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
     // U (or G) from shared memory into A's storage
     for (int r0 = warp; r0 < n; r0 += kT / 32) {
       const int j = sSel[r0];
       const double e = ce[j], f = cf[j];
       const bool fin = !isinf(e);
       // converged: 2^-e g / f = 2^(cs - e) g~ / f; capped: g = 2^cs g~
-      const Pow2 sc(conv ? (fin ? S.cs - static_cast<int>(e) : 0) : S.cs);
+      const Pow2 sc(conv ? (fin ? cs_ - static_cast<int>(e) : 0) : cs_);
       const Divisor d = make_divisor(f);
       const E* x = sG + j * kM;
       E* ucol = Ag + static_cast<int64_t>(r0) * lda;
@@ -337,9 +349,9 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     }
     if (threadIdx.x == 0) {
       if (status_out) status_out[b] = conv ? JSVD_OK : JSVD_ENOCONV;
-      if (sweeps_out) sweeps_out[b] = S.C;
-      if (transforms_out) transforms_out[b] = S.Ttot;
-      if (scale_out) scale_out[b] = S.s;
+      if (sweeps_out) sweeps_out[b] = rC[s];
+      if (transforms_out) transforms_out[b] = sTc[s];
+      if (scale_out) scale_out[b] = rs[s];
     }
     __syncthreads();
   };
@@ -352,42 +364,38 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   int tick = 0;
   for (;;) {
     // finished slots: the pending V rotation, line 41, the next matrix
-    for (int s = 0; s < 2; ++s) {
-      if (sl[s].b < 0 || !sl[s].fin) continue;
-      if (sl[s].pend >= 0) {
-        rotate_v(s, sl[s].pend, (tick - 1) & 1, g, kGroups);
-        __syncthreads();
-      }
-      finalize(s);
-      next(s, sl[s].b + nslots_total);
-    }
-    if (sl[0].b < 0 && sl[1].b < 0) break;
-    mark(6);
-    const int buf = tick & 1;
-    // per-slot step state (uniform): line 6, the Eq. (skr) check (every step
-    // of the flat ordering): in G~'s scale the rescale is a change of cs only
-    bool act[2];
-    int kk[2], cs[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      act[s] = sl[s].b >= 0;
-      kk[s] = sl[s].k;
-      cs[s] = sl[s].cs;
-      if (act[s]) {
-        const int lm = static_cast<int>(sl[s].Mt >> 20) - 1023;
-        if (Kr - lm < 0) {
-          const int sn = Fm - lm - 1;
-          cs[s] += sn;
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            sl[s].Mt = hi32(scalbn_rn(mkd(sl[s].Mt, 0u), sn));
-            sl[s].cs += sn;
-            sl[s].s += sn;
-          }
+      if (rb[s] < 0 || !rfin[s]) continue;
+      if (rfin[s] != 3) {  // (3: handed over -- nothing to finish)
+        if (rpend[s] >= 0) {
+          rotate_v(s, rpend[s], (tick - 1) & 1, g, kGroups);
           __syncthreads();
         }
+        finalize(s);
+      }
+      next(s, rb[s] + nslots_total);
+    }
+    if (rb[0] < 0 && rb[1] < 0) break;
+    mark(6);
+    const int buf = tick & 1;
+    const bool act[2] = {rb[0] >= 0, rb[1] >= 0};
+    // line 6, the Eq. (skr) check (every step of the flat ordering): in G~'s
+    // scale a rescale only moves cs
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!act[s]) continue;
+      const uint32_t mt = sMt[s];
+      const int lm = static_cast<int>(mt >> 20) - 1023;
+      if (Kr - lm < 0) {  // uniform
+        const int sn = Fm - lm - 1;
+        rcs[s] += sn;
+        rs[s] += sn;
+        __syncthreads();  // every thread has read sMt[s]
+        if (threadIdx.x == 0) sMt[s] = hi32(scalbn_rn(mkd(mt, 0u), sn));
       }
     }
+    const int kk[2] = {rk[0], rk[1]};
     // ---- phase A: pair g of both slots, interleaved (raw sums of G~); a
     // group without a pair (n < 32) computes pair 0 and stores nothing, so
     // every lane takes part in the shuffles
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       const bool on = act[s] && l < np;
       Pair& P = sP[(s * 2 + buf) * kGroups + l];
       const double spv = on ? P.sp : 1.0, sqv = on ? P.sq : 1.0;
-      const int c_s = cs[s];
+      const int c_s = rcs[s];
       // R#14 with E := cs (the SSQ of G~ carries 2^(2E - 2cs) exactly)
       const bool zp = !(spv > 0.0), zq = !(sqv > 0.0);
       int iep = kIntMin, ieq = kIntMin;
@@ -485,27 +493,26 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       }
       const unsigned tb = __ballot_sync(kFull, tr), bb = __ballot_sync(kFull, bad);
       if (lane == 0) {
-        sl[0].T += __popc(tb & 0xffffu);
-        sl[1].T += __popc(tb >> 16);
-        sl[0].Ttot += __popc(tb & 0xffffu);
-        sl[1].Ttot += __popc(tb >> 16);
-        if (bb & 0xffffu) sl[0].bad = 1;
-        if (bb >> 16) sl[1].bad = 1;
+        sTc[0] += __popc(tb & 0xffffu);
+        sTc[1] += __popc(tb >> 16);
+        if (bb & 0xffffu) sBad[0] = 1;
+        if (bb >> 16) sBad[1] = 1;
       }
     } else {  // groups 4..15: the V rotations of the previous tick
 #pragma unroll
       for (int s = 0; s < 2; ++s)
-        if (act[s] && sl[s].pend >= 0) rotate_v(s, sl[s].pend, buf ^ 1, g - 4, kGroups - 4);
+        if (act[s] && rpend[s] >= 0) rotate_v(s, rpend[s], buf ^ 1, g - 4, kGroups - 4);
     }
     mark(2);
     __syncthreads();
     mark(3);
+    const bool bad_b[2] = {sBad[0] != 0, sBad[1] != 0};
     // ---- phase C: rotations of G~ (Alg 3.4) and the fast-domain check
     uint32_t Mw0 = 0, Mw1 = 0, lmin0 = ~0u, lmin1 = ~0u;
     if (g < np) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        if (!act[s] || sl[s].bad) continue;
+        if (!act[s] || bad_b[s]) continue;
         const Pair& P = sP[(s * 2 + buf) * kGroups + g];
         if (!P.transform) continue;
         const int p = sPairs[2 * (kk[s] * np + g)], q = sPairs[2 * (kk[s] * np + g) + 1];
@@ -541,45 +548,40 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     Mw0 = __reduce_max_sync(0xffffffffu, Mw0);
     Mw1 = __reduce_max_sync(0xffffffffu, Mw1);
     if (lane == 0) {  // G = G~ 2^cs (normal values)
-      if (Mw0) atomicMax(&sl[0].Mt, Mw0 + (static_cast<uint32_t>(cs[0]) << 20));
-      if (Mw1) atomicMax(&sl[1].Mt, Mw1 + (static_cast<uint32_t>(cs[1]) << 20));
+      if (Mw0) atomicMax(&sMt[0], Mw0 + (static_cast<uint32_t>(rcs[0]) << 20));
+      if (Mw1) atomicMax(&sMt[1], Mw1 + (static_cast<uint32_t>(rcs[1]) << 20));
     }
-    if (lmin0 < kFastLo - 1u) sl[0].bad = 1;
-    if (lmin1 < kFastLo - 1u) sl[1].bad = 1;
+    if (lmin0 < kFastLo - 1u) sBad[0] = 1;
+    if (lmin1 < kFastLo - 1u) sBad[1] = 1;
     mark(4);
     __syncthreads();
     mark(5);
-    // ---- bookkeeping (thread 0): step / sweep counters, convergence
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < 2; ++s) {
-        Slot& S = sl[s];
-        if (!act[s]) continue;
-        if (S.bad) {  // left the fast domain: batched.cu's kernel redoes it
-          reinterpret_cast<unsigned long long*>(sigma)[S.b * n] = kMarker;
-          S.fin = 3;
-          continue;
-        }
-        S.pend = S.k;
-        if (++S.k == n - 1) {  // end of a sweep (line 40)
-          S.k = 0;
-          ++S.C;
-          if (S.T == 0) S.fin = 1;
-          else if (S.C == max_sweeps) S.fin = 2;
-          S.T = 0;
-        }
-      }
-    }
-    __syncthreads();
-    // abandoned slots move on at once (no V rotation, no finalize)
+    // ---- bookkeeping, in every thread: step / sweep counters, line 40
+#pragma unroll
     for (int s = 0; s < 2; ++s) {
-      if (sl[s].b >= 0 && sl[s].fin == 3) next(s, sl[s].b + nslots_total);
+      if (!act[s]) continue;
+      if (sBad[s]) {  // left the fast domain: batched.cu's kernel redoes it
+        if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sigma)[rb[s] * n] = kMarker;
+        rfin[s] = 3;
+        continue;
+      }
+      rpend[s] = rk[s];
+      if (++rk[s] == n - 1) {  // end of a sweep (line 40)
+        rk[s] = 0;
+        ++rC[s];
+        const int tc = sTc[s];
+        if (tc == rT0[s]) rfin[s] = 1;
+        else if (rC[s] == max_sweeps) rfin[s] = 2;
+        rT0[s] = tc;
+      }
     }
     ++tick;
     mark(6);
   }
-  if constexpr (PROF) {
+  if constexpr (PROF) {  // [6]: loads, line 41 and bookkeeping; [7]: the whole kernel
+    pc[7] = pc[0] + pc[1] + pc[2] + pc[3] + pc[4] + pc[5] + pc[6];
     if (lane == 0)
-      for (int k = 0; k < 7; ++k) atomicAdd(&prof[(warp == 0 ? 0 : 1) * 8 + k], pc[k]);
+      for (int k = 0; k < 8; ++k) atomicAdd(&prof[(warp == 0 ? 0 : 1) * 8 + k], pc[k]);
   }
 }
 
