@@ -886,6 +886,16 @@ def run_jsvd(args):
                 "peak_source": peak_src, "kernel": wl.kernel,
                 # SURVEY 8(d).1 reports both: the measured copy peak and the nominal ~8 TB/s
                 "nominal_peak": 8000.0, "nominal_frac": achieved / 8000.0}
+    if args.workload in ("step_r64", "gesvj_r64"):
+        # configs[2]'s G + V (40 MB) stay in the 126 MB L2 across steps, so the
+        # HBM fraction is not the bound: the same algorithmic bytes against a
+        # measured L2-resident copy rate (same footprint), as the ceiling
+        l2 = l2_resident_copy(40 << 20)
+        roofline["l2_ceiling"] = {"achieved": achieved, "peak": l2, "unit": "GB/s",
+                                  "frac": achieved / l2,
+                                  "peak_source": "measured: torch copy_ of a 20 MB buffer into "
+                                                 "another (40 MB, L2-resident), read + write bytes, "
+                                                 "CUDA graph of 200 copies"}
     if isinstance(wl, EvdWorkload) and wl.nsets > 1:  # the short configs[0] launch
         extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
     if isinstance(wl, GesvjWorkload):
@@ -1001,6 +1011,31 @@ def graph_upload(graph, stream):
     rc = cu.cuGraphUpload(ct.c_void_p(graph.raw_cuda_graph_exec()), ct.c_void_p(stream.cuda_stream))
     if rc != 0:
         raise RuntimeError(f"cuGraphUpload failed ({rc})")
+
+
+def l2_resident_copy(footprint):
+    """GB/s (read + write bytes) of a device copy whose source and destination
+    (footprint bytes together) fit in L2, replayed 200 times in a CUDA graph."""
+    import torch
+    half = footprint // 2 // 8
+    a = torch.ones(half, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    b.copy_(a)
+    reps = 200
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            b.copy_(a)
+    torch.cuda.synchronize()
+    graph_upload(g, torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return reps * 2 * half * 8 / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def size_matched_copy(wl, steps, peak):

@@ -120,14 +120,16 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   };
   if constexpr (PROF) tprev = clock64();
 
-  // Per-slot state, uniform over the CTA: every thread keeps its own copy in
-  // registers and updates it identically (no shared-memory round trips on
-  // the per-step path).  Shared: the cumulative transformation count (added
-  // by phase B), the domain flag (set by B and C) and M-tilde (max-reduced
-  // by C).
-  long long rb[2] = {-1, -1};  // matrix (-1: no more work)
-  int rk[2] = {0, 0}, rC[2] = {0, 0}, rs[2] = {0, 0}, rcs[2] = {0, 0};
-  int rpend[2] = {-1, -1}, rfin[2] = {0, 0}, rT0[2] = {0, 0};
+  // Per-slot state in shared memory, written by thread 0 (then a barrier) and
+  // read by every thread at the start of the phase that needs it, so nothing
+  // of it stays live in registers across the phases.  sTc: the cumulative
+  // transformation count (added by phase B); sBad: the domain flag (B, C);
+  // sMt: M-tilde's high word (max-reduced by C).
+  struct SlotSt {
+    long long b;  // matrix (-1: no more work)
+    int k, C, s, cs, pend, fin, T0;
+  };
+  __shared__ SlotSt st[2];
   __shared__ int sTc[2], sBad[2];
   __shared__ uint32_t sMt[2];
 
@@ -200,14 +202,14 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       else v = i == j ? 1.0 : 0.0;
       Vb[static_cast<int64_t>(j) * ldv + i] = v;
     }
-    rb[s] = b;
-    rk[s] = rC[s] = 0;
-    rs[s] = s0;
-    rcs[s] = cs;
-    rpend[s] = -1;
-    rfin[s] = max_sweeps == 0 ? 2 : 0;
-    rT0[s] = 0;
     if (threadIdx.x == 0) {
+      st[s].b = b;
+      st[s].k = st[s].C = 0;
+      st[s].s = s0;
+      st[s].cs = cs;
+      st[s].pend = -1;
+      st[s].fin = max_sweeps == 0 ? 2 : 0;
+      st[s].T0 = 0;
       sMt[s] = hi32(scalbn_rn(M0, s0));
       sBad[s] = 0;
       sTc[s] = 0;
@@ -222,13 +224,14 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       if (load(s, b)) return;
       b += nslots_total;
     }
-    rb[s] = -1;
+    if (threadIdx.x == 0) st[s].b = -1;
+    __syncthreads();
   };
 
   // V rotation of slot s's step kk with the pair parameters in buffer buf:
   // the pairs [l0, np) step ls, lanes of the caller's group
   const auto rotate_v = [&](int s, int kk, int buf, int l0, int ls) {
-    E* Vb = reinterpret_cast<E*>(Vg) + rb[s] * strideV;
+    E* Vb = reinterpret_cast<E*>(Vg) + st[s].b * strideV;
     const Pair* P = sP + (s * 2 + buf) * kGroups;
     for (int l = l0; l < np; l += ls) {
       const Pair& pr = P[l];
@@ -261,8 +264,9 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   // ---- line 41 for slot s: converged -> norms (R#23), U = G diag(2^-e/f),
   // sigma sorted (R#24), V permuted; capped -> G = U Sigma', Sigma' (R#25)
   const auto finalize = [&](int s) {
-    const bool conv = rfin[s] == 1;
-    const int cs_ = rcs[s];
+    const bool conv = st[s].fin == 1;
+    const int cs_ = st[s].cs, s_ = st[s].s;
+    const long long b = st[s].b;
     E* sG = G_of(s);
     double* ce = sE + s * 64;
     double* cf = ce + 32;
@@ -303,12 +307,11 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       sSel[rank] = j;
     }
     __syncthreads();
-    const long long b = rb[s];
     if (threadIdx.x < n) {
       const int r0 = threadIdx.x, j = sSel[r0];
       const double e = ce[j], f = cf[j];
       const bool fin = !isinf(e);
-      const double es = (fin && conv) ? e - rs[s] : e;
+      const double es = (fin && conv) ? e - s_ : e;
       sigma[b * n + r0] = fin ? scalbn_rn(f, static_cast<int>(fmax(fmin(es, 1e5), -1e5))) : 0.0;
     }
     E* Ag = reinterpret_cast<E*>(A) + b * strideA;
@@ -349,9 +352,9 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     }
     if (threadIdx.x == 0) {
       if (status_out) status_out[b] = conv ? JSVD_OK : JSVD_ENOCONV;
-      if (sweeps_out) sweeps_out[b] = rC[s];
+      if (sweeps_out) sweeps_out[b] = st[s].C;
       if (transforms_out) transforms_out[b] = sTc[s];
-      if (scale_out) scale_out[b] = rs[s];
+      if (scale_out) scale_out[b] = s_;
     }
     __syncthreads();
   };
@@ -366,20 +369,22 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     // finished slots: the pending V rotation, line 41, the next matrix
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      if (rb[s] < 0 || !rfin[s]) continue;
-      if (rfin[s] != 3) {  // (3: handed over -- nothing to finish)
-        if (rpend[s] >= 0) {
-          rotate_v(s, rpend[s], (tick - 1) & 1, g, kGroups);
+      const long long b = st[s].b;
+      const int fin = st[s].fin, pend = st[s].pend;
+      if (b < 0 || !fin) continue;
+      if (fin != 3) {  // (3: handed over -- nothing to finish)
+        if (pend >= 0) {
+          rotate_v(s, pend, (tick - 1) & 1, g, kGroups);
           __syncthreads();
         }
         finalize(s);
       }
-      next(s, rb[s] + nslots_total);
+      next(s, b + nslots_total);
     }
-    if (rb[0] < 0 && rb[1] < 0) break;
+    if (st[0].b < 0 && st[1].b < 0) break;
     mark(6);
     const int buf = tick & 1;
-    const bool act[2] = {rb[0] >= 0, rb[1] >= 0};
+    const bool act[2] = {st[0].b >= 0, st[1].b >= 0};
     // line 6, the Eq. (skr) check (every step of the flat ordering): in G~'s
     // scale a rescale only moves cs
 #pragma unroll
@@ -389,13 +394,15 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       const int lm = static_cast<int>(mt >> 20) - 1023;
       if (Kr - lm < 0) {  // uniform
         const int sn = Fm - lm - 1;
-        rcs[s] += sn;
-        rs[s] += sn;
         __syncthreads();  // every thread has read sMt[s]
-        if (threadIdx.x == 0) sMt[s] = hi32(scalbn_rn(mkd(mt, 0u), sn));
+        if (threadIdx.x == 0) {
+          sMt[s] = hi32(scalbn_rn(mkd(mt, 0u), sn));
+          st[s].cs += sn;
+          st[s].s += sn;
+        }
       }
     }
-    const int kk[2] = {rk[0], rk[1]};
+    const int kk[2] = {st[0].k, st[1].k};
     // ---- phase A: pair g of both slots, interleaved (raw sums of G~); a
     // group without a pair (n < 32) computes pair 0 and stores nothing, so
     // every lane takes part in the shuffles
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       const bool on = act[s] && l < np;
       Pair& P = sP[(s * 2 + buf) * kGroups + l];
       const double spv = on ? P.sp : 1.0, sqv = on ? P.sq : 1.0;
-      const int c_s = rcs[s];
+      const int c_s = st[s].cs;
       // R#14 with E := cs (the SSQ of G~ carries 2^(2E - 2cs) exactly)
       const bool zp = !(spv > 0.0), zq = !(sqv > 0.0);
       int iep = kIntMin, ieq = kIntMin;
@@ -500,8 +507,10 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       }
     } else {  // groups 4..15: the V rotations of the previous tick
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
-        if (act[s] && rpend[s] >= 0) rotate_v(s, rpend[s], buf ^ 1, g - 4, kGroups - 4);
+      for (int s = 0; s < 2; ++s) {
+        const int pend = st[s].pend;
+        if (act[s] && pend >= 0) rotate_v(s, pend, buf ^ 1, g - 4, kGroups - 4);
+      }
     }
     mark(2);
     __syncthreads();
@@ -522,19 +531,23 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
         // M-tilde: only pairs with max(e) > K - 1 can reach 2^(K+1) (see step.cu)
         const bool track = max(P.ep, P.eq) > Kr - 1;
         uint32_t Mw = 0, lmin = ~0u;
-        E a[kNR], bq[kNR];
+        constexpr int kH = kNR / 2;  // two halves of the lane's rows (registers)
 #pragma unroll
-        for (int r = 0; r < kNR; ++r) {
-          a[r] = gp[r * kW + hl];
-          bq[r] = gq[r * kW + hl];
-        }
+        for (int h = 0; h < 2; ++h) {
+          E a[kH], bq[kH];
 #pragma unroll
-        for (int r = 0; r < kNR; ++r) {
-          rot_elem(a[r], bq[r], c, Cc, S);
-          gp[r * kW + hl] = a[r];
-          gq[r * kW + hl] = bq[r];
-          lmin = lo_hi_min(a[r], lo_hi_min(bq[r], lmin));
-          if (track) Mw = hi_max(a[r], hi_max(bq[r], Mw));
+          for (int r = 0; r < kH; ++r) {
+            a[r] = gp[(h * kH + r) * kW + hl];
+            bq[r] = gq[(h * kH + r) * kW + hl];
+          }
+#pragma unroll
+          for (int r = 0; r < kH; ++r) {
+            rot_elem(a[r], bq[r], c, Cc, S);
+            gp[(h * kH + r) * kW + hl] = a[r];
+            gq[(h * kH + r) * kW + hl] = bq[r];
+            lmin = lo_hi_min(a[r], lo_hi_min(bq[r], lmin));
+            if (track) Mw = hi_max(a[r], hi_max(bq[r], Mw));
+          }
         }
         if (s == 0) {
           Mw0 = Mw;
@@ -548,33 +561,38 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     Mw0 = __reduce_max_sync(0xffffffffu, Mw0);
     Mw1 = __reduce_max_sync(0xffffffffu, Mw1);
     if (lane == 0) {  // G = G~ 2^cs (normal values)
-      if (Mw0) atomicMax(&sMt[0], Mw0 + (static_cast<uint32_t>(rcs[0]) << 20));
-      if (Mw1) atomicMax(&sMt[1], Mw1 + (static_cast<uint32_t>(rcs[1]) << 20));
+      if (Mw0) atomicMax(&sMt[0], Mw0 + (static_cast<uint32_t>(st[0].cs) << 20));
+      if (Mw1) atomicMax(&sMt[1], Mw1 + (static_cast<uint32_t>(st[1].cs) << 20));
     }
     if (lmin0 < kFastLo - 1u) sBad[0] = 1;
     if (lmin1 < kFastLo - 1u) sBad[1] = 1;
     mark(4);
     __syncthreads();
     mark(5);
-    // ---- bookkeeping, in every thread: step / sweep counters, line 40
+    // ---- bookkeeping (thread 0): step / sweep counters, line 40
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (!act[s]) continue;
-      if (sBad[s]) {  // left the fast domain: batched.cu's kernel redoes it
-        if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sigma)[rb[s] * n] = kMarker;
-        rfin[s] = 3;
-        continue;
-      }
-      rpend[s] = rk[s];
-      if (++rk[s] == n - 1) {  // end of a sweep (line 40)
-        rk[s] = 0;
-        ++rC[s];
-        const int tc = sTc[s];
-        if (tc == rT0[s]) rfin[s] = 1;
-        else if (rC[s] == max_sweeps) rfin[s] = 2;
-        rT0[s] = tc;
+      for (int s = 0; s < 2; ++s) {
+        if (!act[s]) continue;
+        SlotSt t = st[s];
+        if (sBad[s]) {  // left the fast domain: batched.cu's kernel redoes it
+          reinterpret_cast<unsigned long long*>(sigma)[t.b * n] = kMarker;
+          st[s].fin = 3;
+          continue;
+        }
+        t.pend = t.k;
+        if (++t.k == n - 1) {  // end of a sweep (line 40)
+          t.k = 0;
+          ++t.C;
+          const int tc = sTc[s];
+          if (tc == t.T0) t.fin = 1;
+          else if (t.C == max_sweeps) t.fin = 2;
+          t.T0 = tc;
+        }
+        st[s] = t;
       }
     }
+    __syncthreads();
     ++tick;
     mark(6);
   }
