@@ -127,9 +127,13 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   // sMt: M-tilde's high word (max-reduced by C).
   struct SlotSt {
     long long b;  // matrix (-1: no more work)
-    int k, C, s, cs, pend, fin, T0;
+    int s, cs;    // scaling exponents of G and of G~ = G 2^-cs
   };
   __shared__ SlotSt st[2];
+  // the step counters, uniform over the CTA, in every thread's registers:
+  // step, sweep, pending V step, line-40 state (1 converged, 2 capped, 3
+  // handed over) and the transformation count at the sweep's start
+  int rk[2] = {0, 0}, rC[2] = {0, 0}, rpend[2] = {-1, -1}, rfin[2] = {0, 0}, rT0[2] = {0, 0};
   __shared__ int sTc[2], sBad[2];
   __shared__ uint32_t sMt[2];
 
@@ -202,14 +206,13 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       else v = i == j ? 1.0 : 0.0;
       Vb[static_cast<int64_t>(j) * ldv + i] = v;
     }
+    rk[s] = rC[s] = rT0[s] = 0;
+    rpend[s] = -1;
+    rfin[s] = max_sweeps == 0 ? 2 : 0;
     if (threadIdx.x == 0) {
       st[s].b = b;
-      st[s].k = st[s].C = 0;
       st[s].s = s0;
       st[s].cs = cs;
-      st[s].pend = -1;
-      st[s].fin = max_sweeps == 0 ? 2 : 0;
-      st[s].T0 = 0;
       sMt[s] = hi32(scalbn_rn(M0, s0));
       sBad[s] = 0;
       sTc[s] = 0;
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   // ---- line 41 for slot s: converged -> norms (R#23), U = G diag(2^-e/f),
   // sigma sorted (R#24), V permuted; capped -> G = U Sigma', Sigma' (R#25)
   const auto finalize = [&](int s) {
-    const bool conv = st[s].fin == 1;
+    const bool conv = rfin[s] == 1;
     const int cs_ = st[s].cs, s_ = st[s].s;
     const long long b = st[s].b;
     E* sG = G_of(s);
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     }
     if (threadIdx.x == 0) {
       if (status_out) status_out[b] = conv ? JSVD_OK : JSVD_ENOCONV;
-      if (sweeps_out) sweeps_out[b] = st[s].C;
+      if (sweeps_out) sweeps_out[b] = rC[s];
       if (transforms_out) transforms_out[b] = sTc[s];
       if (scale_out) scale_out[b] = s_;
     }
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const long long b = st[s].b;
-      const int fin = st[s].fin, pend = st[s].pend;
+      const int fin = rfin[s], pend = rpend[s];
       if (b < 0 || !fin) continue;
       if (fin != 3) {  // (3: handed over -- nothing to finish)
         if (pend >= 0) {
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
         }
       }
     }
-    const int kk[2] = {st[0].k, st[1].k};
+    const int kk[2] = {rk[0], rk[1]};
     // ---- phase A: pair g of both slots, interleaved (raw sums of G~); a
     // group without a pair (n < 32) computes pair 0 and stores nothing, so
     // every lane takes part in the shuffles
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     } else {  // groups 4..15: the V rotations of the previous tick
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const int pend = st[s].pend;
+        const int pend = rpend[s];
         if (act[s] && pend >= 0) rotate_v(s, pend, buf ^ 1, g - 4, kGroups - 4);
       }
     }
@@ -569,30 +572,26 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     mark(4);
     __syncthreads();
     mark(5);
-    // ---- bookkeeping (thread 0): step / sweep counters, line 40
-    if (threadIdx.x == 0) {
+    // ---- bookkeeping, in every thread (registers): step / sweep counters,
+    // line 40; the next barrier (after phase A) orders the shared state
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (!act[s]) continue;
-        SlotSt t = st[s];
-        if (sBad[s]) {  // left the fast domain: batched.cu's kernel redoes it
-          reinterpret_cast<unsigned long long*>(sigma)[t.b * n] = kMarker;
-          st[s].fin = 3;
-          continue;
-        }
-        t.pend = t.k;
-        if (++t.k == n - 1) {  // end of a sweep (line 40)
-          t.k = 0;
-          ++t.C;
-          const int tc = sTc[s];
-          if (tc == t.T0) t.fin = 1;
-          else if (t.C == max_sweeps) t.fin = 2;
-          t.T0 = tc;
-        }
-        st[s] = t;
+    for (int s = 0; s < 2; ++s) {
+      if (!act[s]) continue;
+      if (sBad[s]) {  // left the fast domain: batched.cu's kernel redoes it
+        if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sigma)[st[s].b * n] = kMarker;
+        rfin[s] = 3;
+        continue;
+      }
+      rpend[s] = rk[s];
+      if (++rk[s] == n - 1) {  // end of a sweep (line 40)
+        rk[s] = 0;
+        ++rC[s];
+        const int tc = sTc[s];
+        if (tc == rT0[s]) rfin[s] = 1;
+        else if (rC[s] == max_sweeps) rfin[s] = 2;
+        rT0[s] = tc;
       }
     }
-    __syncthreads();
     ++tick;
     mark(6);
   }
