@@ -39,7 +39,7 @@ namespace jsvd {
 
 namespace b2 {
 
-constexpr int kT = 128, kW = 8, kNR = 8, kM = 64, kGroups = 16;
+constexpr int kT = 256, kW = 8, kNR = 8, kM = 64, kGroups = 32, kPS = 16;  // kPS: pairs per slot
 constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;  // hi word of 2^-400
 // sigma[b n] of a matrix abandoned to batched.cu's kernel (a NaN payload)
 constexpr unsigned long long kMarker = 0x7ff8badc0ffee123ull;
@@ -92,9 +92,9 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
   const int np = n / 2;
   E* sG0 = reinterpret_cast<E*>(smem_raw);                   // [2][64 n]
   Pair* sP = reinterpret_cast<Pair*>(sG0 + 2 * kM * n);      // [2 slot][2 buf][16]
-  double* sE = reinterpret_cast<double*>(sP + 2 * 2 * kGroups);  // [2][2][32] finalize (e, f)
+  double* sE = reinterpret_cast<double*>(sP + 2 * 2 * kPS);  // [2][2][32] finalize (e, f)
   uint8_t* sPairs = reinterpret_cast<uint8_t*>(sE + 2 * 2 * 32);  // (n-1) x np pivot pairs
-  __shared__ uint64_t wred[4];
+  __shared__ uint64_t wred[kT / 32];
   __shared__ int sSel[32];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -231,32 +231,31 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     __syncthreads();
   };
 
-  // V rotation of slot s's step kk with the pair parameters in buffer buf:
-  // the pairs [l0, np) step ls, lanes of the caller's group
-  const auto rotate_v = [&](int s, int kk, int buf, int l0, int ls) {
+  // V rotation of pair l of slot s's step kk (pair parameters in buffer buf),
+  // by the 8 lanes of the caller's group: 4 rows per lane, loads first
+  const auto rotate_v = [&](int s, int kk, int buf, int l) {
+    const Pair& pr = sP[(s * 2 + buf) * kPS + l];
+    if (!pr.transform) return;
     E* Vb = reinterpret_cast<E*>(Vg) + st[s].b * strideV;
-    const Pair* P = sP + (s * 2 + buf) * kGroups;
-    for (int l = l0; l < np; l += ls) {
-      const Pair& pr = P[l];
-      if (!pr.transform) continue;
-      const int p = sPairs[2 * (kk * np + l)], q = sPairs[2 * (kk * np + l) + 1];
-      E* vp = Vb + static_cast<int64_t>(p) * ldv;
-      E* vq = Vb + static_cast<int64_t>(q) * ldv;
-      constexpr int kRV = 4;  // rows per lane for n <= 32
-      E a[kRV], bq[kRV];
+    const int p = sPairs[2 * (kk * np + l)], q = sPairs[2 * (kk * np + l) + 1];
+    E* vp = Vb + static_cast<int64_t>(p) * ldv;
+    E* vq = Vb + static_cast<int64_t>(q) * ldv;
+    constexpr int kRV = 4;  // rows per lane for n <= 32, two at a time (registers)
+    const double c = pr.c, C = pr.C, S = pr.S;
 #pragma unroll
-      for (int r = 0; r < kRV; ++r) {
-        const int i = r * kW + hl;
-        if (i < n) {
-          a[r] = vp[i];
-          bq[r] = vq[i];
-        }
+    for (int h = 0; h < kRV; h += 2) {
+      E a[2], bq[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {  // (rows past n reread row hl; not stored)
+        const int i = (h + r) * kW + hl < n ? (h + r) * kW + hl : hl;
+        a[r] = vp[i];
+        bq[r] = vq[i];
       }
 #pragma unroll
-      for (int r = 0; r < kRV; ++r) {
-        const int i = r * kW + hl;
+      for (int r = 0; r < 2; ++r) {
+        const int i = (h + r) * kW + hl;
+        rot_elem(a[r], bq[r], c, C, S);
         if (i < n) {
-          rot_elem(a[r], bq[r], pr.c, pr.C, pr.S);
           vp[i] = a[r];
           vq[i] = bq[r];
         }
@@ -377,7 +376,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       if (b < 0 || !fin) continue;
       if (fin != 3) {  // (3: handed over -- nothing to finish)
         if (pend >= 0) {
-          rotate_v(s, pend, (tick - 1) & 1, g, kGroups);
+          if (g < np) rotate_v(s, pend, (tick - 1) & 1, g);
           __syncthreads();
         }
         finalize(s);
@@ -406,51 +405,33 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
       }
     }
     const int kk[2] = {rk[0], rk[1]};
-    // ---- phase A: pair g of both slots, interleaved (raw sums of G~); a
-    // group without a pair (n < 32) computes pair 0 and stores nothing, so
-    // every lane takes part in the shuffles
+    // ---- phase A: group g takes pair g mod 16 of slot g / 16 (raw sums of
+    // G~); a group without a pair (n < 32) computes pair 0 and stores
+    // nothing, so every lane takes part in the shuffles
     {
-      const int ga = g < np ? g : 0;
-      const int p0 = sPairs[2 * (kk[0] * np + ga)], q0 = sPairs[2 * (kk[0] * np + ga) + 1];
-      const int p1 = sPairs[2 * (kk[1] * np + ga)], q1 = sPairs[2 * (kk[1] * np + ga) + 1];
-      const E* gp0 = G_of(0) + p0 * kM;
-      const E* gq0 = G_of(0) + q0 * kM;
-      const E* gp1 = G_of(1) + p1 * kM;
-      const E* gq1 = G_of(1) + q1 * kM;
-      double sp0 = 0.0, sq0 = 0.0, ar0 = 0.0, ai0 = 0.0;
-      double sp1 = 0.0, sq1 = 0.0, ar1 = 0.0, ai1 = 0.0;
+      const int sa = g >> 4, l = g & 15, la = l < np ? l : 0;
+      const int p = sPairs[2 * (kk[sa] * np + la)], q = sPairs[2 * (kk[sa] * np + la) + 1];
+      const E* gp = G_of(sa) + p * kM;
+      const E* gq = G_of(sa) + q * kM;
+      double sp = 0.0, sq = 0.0, ar = 0.0, ai = 0.0;
 #pragma unroll
       for (int r = 0; r < kNR; ++r) {
         const int i = r * kW + hl;
-        const E xp0 = gp0[i], xq0 = gq0[i], xp1 = gp1[i], xq1 = gq1[i];
-        sp0 = ssq_acc(xp0, sp0);
-        sp1 = ssq_acc(xp1, sp1);
-        sq0 = ssq_acc(xq0, sq0);
-        sq1 = ssq_acc(xq1, sq1);
-        dot_acc(xq0, xp0, ar0, ai0);
-        dot_acc(xq1, xp1, ar1, ai1);
+        const E xp = gp[i], xq = gq[i];
+        sp = ssq_acc(xp, sp);
+        sq = ssq_acc(xq, sq);
+        dot_acc(xq, xp, ar, ai);
       }
-      sp0 = hsum<kW>(sp0);
-      sp1 = hsum<kW>(sp1);
-      sq0 = hsum<kW>(sq0);
-      sq1 = hsum<kW>(sq1);
-      ar0 = hsum<kW>(ar0);
-      ar1 = hsum<kW>(ar1);
-      if (CPLX) {
-        ai0 = hsum<kW>(ai0);
-        ai1 = hsum<kW>(ai1);
-      }
-      if (hl == 0 && g < np) {
-        Pair& P0 = sP[(0 * 2 + buf) * kGroups + g];
-        Pair& P1 = sP[(1 * 2 + buf) * kGroups + g];
-        P0.sp = sp0;
-        P0.sq = sq0;
-        P0.ar = ar0;
-        P0.ai = ai0;
-        P1.sp = sp1;
-        P1.sq = sq1;
-        P1.ar = ar1;
-        P1.ai = ai1;
+      sp = hsum<kW>(sp);
+      sq = hsum<kW>(sq);
+      ar = hsum<kW>(ar);
+      if (CPLX) ai = hsum<kW>(ai);
+      if (hl == 0 && l < np) {
+        Pair& P = sP[(sa * 2 + buf) * kPS + l];
+        P.sp = sp;
+        P.sq = sq;
+        P.ar = ar;
+        P.ai = ai;
       }
     }
     mark(0);
@@ -460,7 +441,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
     if (warp == 0) {
       const int s = lane >> 4, l = lane & 15;
       const bool on = act[s] && l < np;
-      Pair& P = sP[(s * 2 + buf) * kGroups + l];
+      Pair& P = sP[(s * 2 + buf) * kPS + l];
       const double spv = on ? P.sp : 1.0, sqv = on ? P.sq : 1.0;
       const int c_s = st[s].cs;
       // R#14 with E := cs (the SSQ of G~ carries 2^(2E - 2cs) exactly)
@@ -508,35 +489,32 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
         if (bb & 0xffffu) sBad[0] = 1;
         if (bb >> 16) sBad[1] = 1;
       }
-    } else {  // groups 4..15: the V rotations of the previous tick
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int pend = rpend[s];
-        if (act[s] && pend >= 0) rotate_v(s, pend, buf ^ 1, g - 4, kGroups - 4);
+    } else {  // groups 4..31: the V rotations of the previous tick (both slots)
+      for (int lv = g - 4; lv < 2 * kPS; lv += kGroups - 4) {
+        const int s = lv >> 4, l = lv & 15;
+        if (l < np && act[s] && rpend[s] >= 0) rotate_v(s, rpend[s], buf ^ 1, l);
       }
     }
     mark(2);
     __syncthreads();
     mark(3);
     const bool bad_b[2] = {sBad[0] != 0, sBad[1] != 0};
-    // ---- phase C: rotations of G~ (Alg 3.4) and the fast-domain check
-    uint32_t Mw0 = 0, Mw1 = 0, lmin0 = ~0u, lmin1 = ~0u;
-    if (g < np) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (!act[s] || bad_b[s]) continue;
-        const Pair& P = sP[(s * 2 + buf) * kGroups + g];
-        if (!P.transform) continue;
-        const int p = sPairs[2 * (kk[s] * np + g)], q = sPairs[2 * (kk[s] * np + g) + 1];
-        E* gp = G_of(s) + p * kM;
-        E* gq = G_of(s) + q * kM;
+    // ---- phase C: rotations of G~ (Alg 3.4) and the fast-domain check;
+    // warps 0-3 hold slot 0's groups, warps 4-7 slot 1's
+    {
+      const int sc_ = g >> 4, l = g & 15;
+      uint32_t Mw = 0, lmin = ~0u;
+      const Pair& P = sP[(sc_ * 2 + buf) * kPS + l];
+      if (l < np && act[sc_] && !bad_b[sc_] && P.transform) {
+        const int p = sPairs[2 * (kk[sc_] * np + l)], q = sPairs[2 * (kk[sc_] * np + l) + 1];
+        E* gp = G_of(sc_) + p * kM;
+        E* gq = G_of(sc_) + q * kM;
         const double c = P.c, Cc = P.C, S = P.S;
         // M-tilde: only pairs with max(e) > K - 1 can reach 2^(K+1) (see step.cu)
         const bool track = max(P.ep, P.eq) > Kr - 1;
-        uint32_t Mw = 0, lmin = ~0u;
-        constexpr int kH = kNR / 2;  // two halves of the lane's rows (registers)
+        constexpr int kH = kNR / 4;  // a quarter of the lane's rows at a time (registers)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kNR / kH; ++h) {
           E a[kH], bq[kH];
 #pragma unroll
           for (int r = 0; r < kH; ++r) {
@@ -552,23 +530,11 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
             if (track) Mw = hi_max(a[r], hi_max(bq[r], Mw));
           }
         }
-        if (s == 0) {
-          Mw0 = Mw;
-          lmin0 = lmin;
-        } else {
-          Mw1 = Mw;
-          lmin1 = lmin;
-        }
       }
+      Mw = __reduce_max_sync(0xffffffffu, Mw);
+      if (lane == 0 && Mw) atomicMax(&sMt[sc_], Mw + (static_cast<uint32_t>(st[sc_].cs) << 20));
+      if (lmin < kFastLo - 1u) sBad[sc_] = 1;  // G = G~ 2^cs above (normal values)
     }
-    Mw0 = __reduce_max_sync(0xffffffffu, Mw0);
-    Mw1 = __reduce_max_sync(0xffffffffu, Mw1);
-    if (lane == 0) {  // G = G~ 2^cs (normal values)
-      if (Mw0) atomicMax(&sMt[0], Mw0 + (static_cast<uint32_t>(st[0].cs) << 20));
-      if (Mw1) atomicMax(&sMt[1], Mw1 + (static_cast<uint32_t>(st[1].cs) << 20));
-    }
-    if (lmin0 < kFastLo - 1u) sBad[0] = 1;
-    if (lmin1 < kFastLo - 1u) sBad[1] = 1;
     mark(4);
     __syncthreads();
     mark(5);
@@ -604,7 +570,7 @@ __global__ void __launch_bounds__(kT, 3) batched2_kernel(
 
 size_t batched2_smem(bool cplx, int64_t n) {
   const size_t w = cplx ? 16 : 8;
-  return w * 2 * kM * n + sizeof(Pair) * 2 * 2 * kGroups + sizeof(double) * 2 * 2 * 32 +
+  return w * 2 * kM * n + sizeof(Pair) * 2 * 2 * kPS + sizeof(double) * 2 * 2 * 32 +
          2 * (n - 1) * (n / 2);
 }
 
