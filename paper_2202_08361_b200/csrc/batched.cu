@@ -722,7 +722,9 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
   // same results bit for bit -- the GPU tests compare both)
   const char* fast_s = getenv("JSVD_BATCHED_FAST");
   const bool fast_env = !fast_s || atoi(fast_s) != 0;
-  if (fast_env && batched2_ok(m, n)) {
+  const char* b2_s = getenv("JSVD_BATCHED2");  // 0: the one-matrix kernel below (A/B runs)
+  const bool b2_env = !b2_s || atoi(b2_s) != 0;
+  if (fast_env && b2_env && batched2_ok(m, n)) {
     // configs[3]'s shape: the persistent two-slot kernel (batched2.cu), then
     // this kernel, in G's own scale, on the matrices it handed over
     e = launch_batched2(cplx, batch, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps,
@@ -735,8 +737,10 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
   }
   auto pick = [&](auto cplx_t) {
     constexpr bool C = decltype(cplx_t)::value;
-    if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true, false>, 128);
+    if (prof && fast_env) go16(batched_svd_kernel<C, 8, true, 8, 16, true, true>, 128);
+    else if (prof) go16(batched_svd_kernel<C, 8, true, 8, 16, true, false>, 128);
     else if (m == 32) go(batched_svd_kernel<C, 4, true, 8>, 128);
+    else if (m == 64 && vh16 && fast_env && !marked) go16(batched_svd_kernel<C, 8, true, 8, 16>, 128);
     else if (m == 64 && vh16) go16(batched_svd_kernel<C, 8, true, 8, 16, false, false>, 128);
     else if (m == 64) go(batched_svd_kernel<C, 8, true, 8>, 128);
     else if (m < 32) go(batched_svd_kernel<C, 4, false, 8>, 128);
