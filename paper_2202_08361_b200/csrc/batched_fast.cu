@@ -38,10 +38,10 @@ constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;  // hi wor
 constexpr unsigned long long kMarker = 0x7ff8badc0ffee123ull;
 
 struct Pair {
-  double zr, zi, fp, fq;  // A: the scaled dot a21' (Alg 3.1) and the norms' f
+  double ar, ai, sp, sq;  // A: raw sums of G~ (dot, SSQ of p and q)
   double c, C, S;         // B: rotation
-  int ep, eq;             // A: norm exponents (kIntMin: zero column)
-  int transform, pad;     // A: Alg 3.2
+  int ep, eq;             // B: norm exponents (kIntMin: zero column)
+  int transform, pad;
 };
 
 __device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
@@ -257,51 +257,48 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
       sq = hsum<kW>(sq);
       ar = hsum<kW>(ar);
       if (CPLX) ai = hsum<kW>(ai);
-      // the pair's scalar tail up to Alg 3.2, in every lane of the group (the
-      // butterfly left the sums in all of them): R#14 with E := cs (the SSQ
-      // of G~ carries 2^(2E - 2cs) exactly), the dot's rescale by
-      // 2^(2cs - e_q - e_p) (exact), its division (Alg 3.1 line 8), the test
-      const bool zp = !(sp > 0.0), zq = !(sq > 0.0);
-      int iep = kIntMin, ieq = kIntMin;
-      double gpv = 1.0, gqv = 1.0;
-      if (!zp) eg_of(cs, sp, iep, gpv);
-      if (!zq) eg_of(cs, sq, ieq, gqv);
-      if (!(zp || zq)) {
-        const double f2 = pow2i(2 * cs - iep - ieq);
-        ar *= f2;
-        ai *= f2;
-      }
-      const double fp = zp ? 1.0 : sqrt_plain(gpv), fq = zq ? 1.0 : sqrt_plain(gqv);
-      const Rcp d = rcp_plain(fq * fp);
-      const double zr = dot_div(ar, d, kFull);
-      const double zi = CPLX ? dot_div(ai, d, kFull) : 0.0;
-      const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
-      const bool tr = !(zp || zq) && tol <= az;  // Alg 3.2
       if (hl == 0 && g < np) {
         Pair& P = sP[buf * kG + g];
-        P.zr = zr;
-        P.zi = zi;
-        P.fp = fp;
-        P.fq = fq;
-        P.ep = iep;
-        P.eq = ieq;
-        P.transform = tr;
+        P.sp = sp;
+        P.sq = sq;
+        P.ar = ar;
+        P.ai = ai;
       }
     }
     mark(0);
     __syncthreads();
     mark(1);
     // ---- phase B (warp 0, lane l: pair l) | V of the previous step (warps 1-3)
-    if (warp == 0) {  // Grammian (Alg 3.3) and 2x2 EVD (Alg 2.2) of the step's pairs
+    if (warp == 0) {
       const int l = lane;
-      Pair& P = sP[buf * kG + (l < np ? l : 0)];
-      const bool tr = l < np && P.transform;
+      const bool on = l < np;
+      Pair& P = sP[buf * kG + (on ? l : 0)];
+      const double spv = on ? P.sp : 1.0, sqv = on ? P.sq : 1.0;
+      // R#14 with E := cs (the SSQ of G~ carries 2^(2E - 2cs) exactly)
+      const bool zp = !(spv > 0.0), zq = !(sqv > 0.0);
+      int iep = kIntMin, ieq = kIntMin;
+      double gp = 1.0, gq = 1.0;
+      if (!zp) eg_of(cs, spv, iep, gp);
+      if (!zq) eg_of(cs, sqv, ieq, gq);
+      double arv = on ? P.ar : 0.0, aiv = on ? P.ai : 0.0;
+      if (!(zp || zq)) {  // the dot of G~ carries 2^(2cs - e_q - e_p) exactly
+        const double f2 = pow2i(2 * cs - iep - ieq);
+        arv *= f2;
+        aiv *= f2;
+      }
+      const double fp = zp ? 1.0 : sqrt_plain(gp), fq = zq ? 1.0 : sqrt_plain(gq);
+      const double ep = zp ? -INFINITY : static_cast<double>(iep);
+      const double eq = zq ? -INFINITY : static_cast<double>(ieq);
+      const Rcp d = rcp_plain(fq * fp);  // Alg 3.1 line 8
+      const double zr = dot_div(arv, d, kFull);
+      const double zi = CPLX ? dot_div(aiv, d, kFull) : 0.0;
+      const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
+      const bool tr = on && !(zp || zq) && tol <= az;  // Alg 3.2
       bool bad = false;
       if (__any_sync(kFull, tr)) {
         double b11, b22, br, bi;
-        gram_fast(tr ? P.zr : 0.0, tr ? P.zi : 0.0, tr ? static_cast<double>(P.ep) : 0.0,
-                  tr ? P.fp : 1.0, tr ? static_cast<double>(P.eq) : 0.0, tr ? P.fq : 1.0, b11,
-                  b22, br, bi, kFull);
+        gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
+                  tr ? fq : 1.0, b11, b22, br, bi, kFull);
         const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);
         if (tr) {
           P.c = o.c;
@@ -309,6 +306,11 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
           P.S = o.si;
           bad = (abs_hi(o.sr) - 1u < kFastLo - 1u) || (abs_hi(o.si) - 1u < kFastLo - 1u);
         }
+      }
+      if (on) {
+        P.transform = tr;
+        P.ep = iep;
+        P.eq = ieq;
       }
       const unsigned tb = __ballot_sync(kFull, tr), bb = __ballot_sync(kFull, bad);
       if (lane == 0) {
