@@ -37,11 +37,11 @@ namespace jsvd {
 // nonzero values below 2^-1022 cannot occur in fast mode (their rotation
 // inputs are >= 2^-400, so every nonzero output is >= 2^-905).
 constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;
-// sigma[b n] of a matrix batched2.cu's kernel hands over to this one
-constexpr unsigned long long kBatched2Marker = 0x7ff8badc0ffee123ull;
-size_t batched2_smem(bool cplx, int64_t n);
-bool batched2_ok(int64_t m, int64_t n);
-cudaError_t launch_batched2(bool cplx, int64_t batch, int64_t n, double* A, int64_t lda,
+// sigma[b n] of a matrix batched_fast.cu's kernel hands over to this one
+constexpr unsigned long long kFastMarker = 0x7ff8badc0ffee123ull;
+size_t batched_fast_smem(bool cplx, int64_t n);
+bool batched_fast_ok(int64_t m, int64_t n);
+cudaError_t launch_batched_fast(bool cplx, int64_t batch, int64_t n, double* A, int64_t lda,
                             int64_t strideA, double* V, int64_t ldv, int64_t strideV,
                             double* sigma, int max_sweeps, int32_t* sweeps, int32_t* status,
                             int64_t* transforms, int32_t* scale, int Fm, int Kr, double tol,
@@ -163,9 +163,9 @@ __global__ void __launch_bounds__(16 * W, W == 8 ? 5 : 2) batched_svd_kernel(
   __shared__ int sSel[64];  // finalize: input column of each output rank
 
   const int64_t b = blockIdx.x;
-  // after batched2.cu's kernel: only the matrices it handed over
+  // after batched_fast.cu's kernel: only the matrices it handed over
   if (marked_only &&
-      reinterpret_cast<const unsigned long long*>(sigma)[b * n] != kBatched2Marker)
+      reinterpret_cast<const unsigned long long*>(sigma)[b * n] != kFastMarker)
     return;
   E* Ag = reinterpret_cast<E*>(A) + b * strideA;
   E* Vb = reinterpret_cast<E*>(Vg) + b * strideV;
@@ -688,7 +688,7 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
   if ((opts && opts->max_steps) || adj < -2200 || adj > 1024 - Fm) return JSVD_EINVAL;
   const double tol = std::ldexp(std::sqrt(static_cast<double>(m)), -53);
   cudaError_t e;
-  int marked = 0;  // 1: only the matrices batched2.cu's kernel handed over
+  int marked = 0;  // 1: only the matrices batched_fast.cu's kernel handed over
   auto go = [&](auto kern, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<static_cast<unsigned>(batch), threads, smem, st>>>(m, n, A, lda, strideA, V, ldv, strideV,
@@ -722,12 +722,12 @@ static jsvd_status batched_impl(jsvd_dtype dt, int64_t batch, int64_t m, int64_t
   // same results bit for bit -- the GPU tests compare both)
   const char* fast_s = getenv("JSVD_BATCHED_FAST");
   const bool fast_env = !fast_s || atoi(fast_s) != 0;
-  const char* b2_s = getenv("JSVD_BATCHED2");  // 0: the one-matrix kernel below (A/B runs)
+  const char* b2_s = getenv("JSVD_BATCHED_KERNEL");  // 0: batched.cu's kernel for configs[3] too (A/B runs)
   const bool b2_env = !b2_s || atoi(b2_s) != 0;
-  if (fast_env && b2_env && batched2_ok(m, n)) {
-    // configs[3]'s shape: the persistent two-slot kernel (batched2.cu), then
+  if (fast_env && b2_env && batched_fast_ok(m, n)) {
+    // configs[3]'s shape: the persistent two-slot kernel (batched_fast.cu), then
     // this kernel, in G's own scale, on the matrices it handed over
-    e = launch_batched2(cplx, batch, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps,
+    e = launch_batched_fast(cplx, batch, n, A, lda, strideA, V, ldv, strideV, sigma, max_sweeps,
                         sweeps_done, status, transforms, scale, Fm, Kr, tol, adj, prof, st);
     if (e != cudaSuccess) return JSVD_ECUDA;
     marked = 1;

@@ -475,21 +475,21 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
   }
 }
 
-size_t batched2_smem(bool cplx, int64_t n) {
+size_t batched_fast_smem(bool cplx, int64_t n) {
   const size_t w = cplx ? 16 : 8;
   return w * kM * n + sizeof(Pair) * 2 * kG + sizeof(double) * 64 + 2 * (n - 1) * (n / 2);
 }
 
-bool batched2_ok(int64_t m, int64_t n) { return m == kM && n >= 2 && n <= 32 && (n & 1) == 0; }
+bool batched_fast_ok(int64_t m, int64_t n) { return m == kM && n >= 2 && n <= 32 && (n & 1) == 0; }
 
 // one CTA per matrix; `prof` (16 uint64, zeroed by the caller) selects the
 // clock64-instrumented build
-cudaError_t launch_batched2(bool cplx, int64_t batch, int64_t n, double* A, int64_t lda,
+cudaError_t launch_batched_fast(bool cplx, int64_t batch, int64_t n, double* A, int64_t lda,
                             int64_t strideA, double* V, int64_t ldv, int64_t strideV,
                             double* sigma, int max_sweeps, int32_t* sweeps, int32_t* status,
                             int64_t* transforms, int32_t* scale, int Fm, int Kr, double tol,
                             int adj, unsigned long long* prof, cudaStream_t st) {
-  const size_t smem = batched2_smem(cplx, n);
+  const size_t smem = batched_fast_smem(cplx, n);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
