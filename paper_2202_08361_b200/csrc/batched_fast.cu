@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
     sPairs[2 * k + 1] = static_cast<uint8_t>(q);
   }
 
+  // @phase load
   // ---- load A; M0 = max |component| (NaN -> inf), mn = the smallest nonzero
   uint64_t mx = 0, mn = ~0ull;
   {
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
   }
   __syncthreads();
 
+  // @phase star:V
   // V rotation of pair l of step kk (parameters in buffer buf), by the 8
   // lanes of the caller's group: 4 rows per lane, two at a time
   const auto rotate_v = [&](int kk, int buf, int l) {
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
   int k = 0, C = 0, pend = -1, pend_buf = 0, T0 = 0, fin = max_sweeps == 0 ? 2 : 0;
   for (int tick = 0; !fin; ++tick) {
     const int buf = tick & 1;
+    // @phase rescale-check
     // line 6, the Eq. (skr) check (every step of the flat ordering): in G~'s
     // scale a rescale only moves cs
     {
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
         if (threadIdx.x == 0) sMt = hi32(scalbn_rn(mkd(mt, 0u), sn));
       }
     }
+    // @phase A:spade+club
     // ---- phase A (a group without a pair, n < 32, computes pair 0 and
     // stores nothing, so every lane takes part in the shuffles)
     {
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
     mark(0);
     __syncthreads();
     mark(1);
+    // @phase B:heart+diamond
     // ---- phase B (warp 0, lane l: pair l) | V of the previous step (warps 1-3)
     if (warp == 0) {
       const int l = lane;
@@ -317,12 +322,14 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
         sT += __popc(tb);
         if (bb) sBad = 1;
       }
+    // @phase star:V
     } else if (pend >= 0) {  // groups 4..15: V of the previous step
       for (int l = g - 4; l < np; l += kG - 4) rotate_v(pend, buf ^ 1, l);
     }
     mark(2);
     __syncthreads();
     mark(3);
+    // @phase C:star-G
     if (sBad) break;  // a C or S below 2^-400: hand the matrix over (uniform)
     // ---- phase C: the rotation of G~'s pair g (Alg 3.4), the domain check
     {
@@ -362,6 +369,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
     __syncthreads();
     mark(5);
     if (sBad) break;  // a rotated value below 2^-400 (uniform)
+    // @phase bookkeeping
     // ---- step / sweep counters (every thread), line 40
     pend = k;
     pend_buf = buf;
@@ -384,6 +392,7 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
     if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sigma)[b * n] = kMarker;
     return;
   }
+  // @phase line41
   if (pend >= 0) {  // the last step's V rotation
     if (g < np) rotate_v(pend, pend_buf, g);
     __syncthreads();

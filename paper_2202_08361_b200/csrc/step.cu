@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   E* gq = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(q) * P.ldg;
   const bool lead = (crank == 0) && (threadIdx.x == 0);
 
+  // @phase load+rescale
   // the shared-memory rows first (asynchronous), then the register rows
 #pragma unroll 2
   for (int j = 0; j < NS; ++j) {
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
   }
 
+  // @phase spade:norms
   // ---- spade: E = floor(lg max |component|) per column (high words)
   uint32_t hp = 0, hq = 0;
 #pragma unroll
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     P.col_f[q] = fq;
   }
 
+  // @phase club:dot
   // ---- club: a21' = (g_q 2^-e_q)^* (g_p 2^-e_p) / fl(f_q f_p)  (Alg 3.1)
   double zr = 0.0, zi = 0.0;
   const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19 (cluster-uniform)
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   if constexpr (CL > 1) {
     if (!zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   }
+  // @phase heart:test+V-prefetch
   // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
   const double az = CPLX ? hypot_naive(fabs(zr), fabs(zi)) : fabs(zr);
   const bool transform = P.tol <= az;
@@ -280,6 +284,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
   }
 
+  // @phase heart+diamond:Gram+EVD
   if (transform) {
     if (threadIdx.x < 32) {  // heart + diamond, computed by one warp per CTA
       double b11, b22, br, bi;
@@ -293,6 +298,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
     __syncthreads();
     const double c = rot[0], C = rot[1], S = rot[2];
+    // @phase star:rotate-G
     // ---- star: rotate the pair (registers; shared rows back in place)
 #pragma unroll
     for (int j = 0; j < NR; ++j) rot_elem(xp[j], xq[j], c, C, S);
@@ -322,6 +328,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       }
     }
   }
+  // @phase star:rotate-V
   if (transform) {
     if (P.V) {
       const double c = rot[0], C = rot[1], S = rot[2];
@@ -341,6 +348,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
         vq[i] = b;
       }
     }
+    // @phase M+bookkeeping
     // ---- M: max |component| of the transformed pair.  In the driver
     // (Mt) only floor(lg M-tilde) >= K + 1 matters (Eq. skr): every component
     // is below sqrt(|g_p|^2 + |g_q|^2) <= 2^(max(e_p,e_q) + 1.5), so a pair
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   }
 }
 
+// @phase finalize
 // ---- finalize helpers ---------------------------------------
 // norms of all columns with the same code and lane order as the step (R#23)
 template <bool CPLX, int T, int CL, int NR>
