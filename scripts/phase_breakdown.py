@@ -47,7 +47,8 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", cub, os.path.abspath(lib)], cwd=tmp, capture_output=True)
 dis = subprocess.run(["nvdisasm", "-gi", os.path.join(tmp, cub)], capture_output=True,
                      text=True).stdout
-line_at, inside, pending, last = {}, False, [], None
+line_at, inside, pending, last, saw_loc = {}, False, [], None, False
+# (an instruction with no location in SOURCE keeps last = None: "outside")
 for l in dis.splitlines():
     m = re.match(r"\s*\.section\s+\.text\.(\S+),", l)
     if m:
@@ -57,22 +58,23 @@ for l in dis.splitlines():
     if not inside:
         continue
     if "//##" in l:
+        saw_loc = True
         for f, n in re.findall(r'"([^"]+)", line (\d+)', l):
             if os.path.basename(f) == srcname:
                 pending.append(int(n))
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", l)
     if m:
+        line_at[int(m.group(1), 16)] = pending[-1] if pending else (last if not saw_loc else None)
         if pending:
             last = pending[-1]
-        pending = []
-        line_at[int(m.group(1), 16)] = last
+        pending, saw_loc = [], False
 
 agg = collections.defaultdict(lambda: [0.0, 0.0])
 ts = te = 0.0
 for a, s, e in prof:
     ln = line_at.get(a - base)
-    ph = phase_of_line.get(ln, "prologue") if ln else "?"
+    ph = phase_of_line.get(ln, "prologue") if ln else f"outside {srcname}"
     agg[ph][0] += s
     agg[ph][1] += e
     ts += s
