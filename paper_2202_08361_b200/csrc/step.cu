@@ -13,7 +13,6 @@
 //   star   rotation of g_p, g_q in registers + store, then v_p, v_q (Alg 3.4)
 // so G is read once and written once per transformed pair, V read+written
 // once per transformed pair, nothing for a converged pair (R#26: no max on V).
-#include <cstdlib>
 #include <mutex>
 #include <vector>
 #include <utility>
@@ -48,8 +47,8 @@ __device__ __forceinline__ double2 scalbn_el(double2 x, int n) {
 // twice the rows per lane at the same register count, so a pair needs half the
 // CTAs and twice as many pairs are resident).  Every pass walks j upwards, so
 // the per-lane accumulation order of R is unchanged.
-template <bool CPLX, int T, int CL, int NR, int NS, int MINB = 2>
-__global__ void __launch_bounds__(T, MINB) step_kernel(const StepParams P) {
+template <bool CPLX, int T, int CL, int NR, int NS>
+__global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   using E = typename Elem<CPLX>::T;
   constexpr int W = T * CL;
   constexpr int NW = T / 32;
@@ -531,17 +530,6 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
   return e;
 }
 
-static int sm_count() {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
-static bool step_smem_env() {
-  const char* e = getenv("JSVD_STEP_SMEM");
-  return !e || atoi(e) != 0;
-}
-
 template <bool CPLX>
 static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams& P,
                                  cudaStream_t st) {
@@ -558,16 +546,6 @@ static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams&
       case 16: return launch_cl(step_kernel<CPLX, 256, 16, NRr, NSs>, grid, 256, 16, sm, st, true, P);
     }
     return cudaErrorInvalidValue;
-  }
-  // single-CTA pairs with long columns (m > 256 NR/2) and more pairs than two
-  // CTAs per SM hold: half of each lane's rows in shared memory (32 KB per
-  // CTA, <= 64 registers), so four CTAs fit per SM and configs[2]'s 512 pairs
-  // run in one wave on 148 SMs instead of 1.7 -- the same lane order R, so the
-  // same bits (JSVD_STEP_SMEM=0 keeps the register-only kernel, for A/B runs)
-  if (g.CL == 1 && P.m > 256 * (NR / 2) && npairs > 2 * sm_count() && step_smem_env()) {
-    constexpr int NH = NR / 2;
-    const size_t smh = static_cast<size_t>(NH) * 2 * 256 * sizeof(E);
-    return launch_cl(step_kernel<CPLX, 256, 1, NH, NH, 4>, grid, 256, 1, smh, st, true, P);
   }
   switch (g.CL) {
     case 1: return launch_cl(step_kernel<CPLX, 256, 1, NR, 0>, grid, 256, 1, 0, st, true, P);
