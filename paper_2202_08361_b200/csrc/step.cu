@@ -21,6 +21,10 @@
 #include "step_dev.cuh"
 #include "step_params.h"
 
+#ifndef JSVD_STEP_NV_REAL
+#define JSVD_STEP_NV_REAL 4
+#endif
+
 namespace jsvd {
 
 // 16-byte / 8-byte asynchronous global -> shared copies (LDGSTS), zero-filled
@@ -268,8 +272,9 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   const bool transform = P.tol <= az;
 
   // V columns of a transformed pair: the first NV rows per lane are loaded
-  // now, so their latency overlaps the Grammian + EVD of warp 0
-  constexpr int NV = 2;
+  // now, so their latency overlaps the Grammian + EVD of warp 0 (real single
+  // CTAs: 4 rows -- all of configs[2]'s V with W = 256 lanes)
+  constexpr int NV = (!CPLX && CL == 1 && NS == 0) ? (JSVD_STEP_NV_REAL) : 2;
   E va[NV], vb[NV];
   E* vp = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(p) * P.ldv;
   E* vq = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(q) * P.ldv;
