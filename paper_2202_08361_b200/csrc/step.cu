@@ -24,6 +24,9 @@
 #ifndef JSVD_STEP_NV_REAL
 #define JSVD_STEP_NV_REAL 4
 #endif
+#ifndef JSVD_STEP_NV_CPLX
+#define JSVD_STEP_NV_CPLX 4
+#endif
 
 namespace jsvd {
 
@@ -274,7 +277,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   // V columns of a transformed pair: the first NV rows per lane are loaded
   // now, so their latency overlaps the Grammian + EVD of warp 0 (real single
   // CTAs: 4 rows -- all of configs[2]'s V with W = 256 lanes)
-  constexpr int NV = (!CPLX && CL == 1 && NS == 0) ? (JSVD_STEP_NV_REAL) : 2;
+  constexpr int NV = (!CPLX && CL == 1 && NS == 0) ? (JSVD_STEP_NV_REAL)
+                     : (CPLX && NS > 0) ? (JSVD_STEP_NV_CPLX) : 2;
   E va[NV], vb[NV];
   E* vp = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(p) * P.ldv;
   E* vq = reinterpret_cast<E*>(P.V) + static_cast<int64_t>(q) * P.ldv;
