@@ -32,11 +32,9 @@
 namespace jsvd {
 
 // Fast mode: every value of G~ is 0 or has |x| >= 2^-400,
-// i.e. a high word (sign masked) of at least kFastLo.  lo_hi_min folds
-// hi(|x|) - 1 into a running minimum: 0 maps to 0xffffffff and passes;
-// nonzero values below 2^-1022 cannot occur in fast mode (their rotation
-// inputs are >= 2^-400, so every nonzero output is >= 2^-905).
-constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;
+// i.e. a high word (sign masked) of at least kFastLo (step_dev.cuh; nonzero
+// values below 2^-1022 cannot occur in fast mode: their rotation inputs are
+// >= 2^-400, so every nonzero output is >= 2^-905).
 // sigma[b n] of a matrix batched_fast.cu's kernel hands over to this one
 constexpr unsigned long long kFastMarker = 0x7ff8badc0ffee123ull;
 size_t batched_fast_smem(bool cplx, int64_t n);
@@ -46,12 +44,6 @@ cudaError_t launch_batched_fast(bool cplx, int64_t batch, int64_t n, double* A, 
                             double* sigma, int max_sweeps, int32_t* sweeps, int32_t* status,
                             int64_t* transforms, int32_t* scale, int Fm, int Kr, double tol,
                             int adj, unsigned long long* prof, cudaStream_t st);
-__device__ __forceinline__ uint32_t lo_hi_min(double x, uint32_t m) {
-  return min(m, abs_hi(x) - 1u);
-}
-__device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
-  return min(m, min(abs_hi(x.x) - 1u, abs_hi(x.y) - 1u));
-}
 
 // W lanes per pair (R.W = 8 for m <= 64, 16 above) and 16 lane groups per CTA
 // (16 W threads): one pass of phases A and C covers the 16 pairs of n = 32

@@ -33,7 +33,6 @@ namespace jsvd {
 namespace bf {
 
 constexpr int kT = 128, kW = 8, kNR = 8, kM = 64, kG = 16;
-constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;  // hi word of 2^-400
 // sigma[b n] of a matrix handed to batched.cu's kernel (a NaN payload)
 constexpr unsigned long long kMarker = 0x7ff8badc0ffee123ull;
 
@@ -44,10 +43,6 @@ struct Pair {
   int transform, pad;
 };
 
-__device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
-  return min(m, min(abs_hi(x.x) - 1u, abs_hi(x.y) - 1u));
-}
-__device__ __forceinline__ uint32_t lo_hi_min(double x, uint32_t m) { return min(m, abs_hi(x) - 1u); }
 
 template <int W>
 __device__ __forceinline__ double hsum(double v) {

@@ -35,6 +35,7 @@ cudaError_t launch_colnorm(bool cplx, int64_t m, int64_t n, const double* G, int
                            double* ce, double* cf, cudaStream_t st);
 bool step_supported(bool cplx, int64_t m);
 bool strategy_ok(int64_t n, int64_t B);
+bool step_fast_enabled();
 
 struct WsHeader {
   unsigned long long Mt[3];
@@ -504,6 +505,7 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
   P.s_slots = hdr->s;
   P.Fm = Fm;
   P.Kr = cplx ? 1020 : 1022;
+  P.fast = step_fast_enabled() ? 1 : 0;
   // col_e/col_f of the step are indexed by local column: sized nl
 
   // the block moves after a phase-II round (position k -> k-1, 1 -> B-1, 0

@@ -13,6 +13,7 @@
 //   star   rotation of g_p, g_q in registers + store, then v_p, v_q (Alg 3.4)
 // so G is read once and written once per transformed pair, V read+written
 // once per transformed pair, nothing for a converged pair (R#26: no max on V).
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 #include <utility>
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   __shared__ uint32_t rs_m[NW];
   __shared__ double rot[3];
   __shared__ TxSlot<CL, int> tx_e;
-  __shared__ TxSlot<CL, double> tx_ssq, tx_dot;
+  __shared__ TxSlot<CL, double> tx_ssq, tx_dot, tx_f1, tx_f2;
+  __shared__ RedSlot<NW, double> rs_f1, rs_f2;
   extern __shared__ __align__(16) unsigned char step_smem[];
   E* sx = reinterpret_cast<E*>(step_smem);  // [NS][2][T]
   const auto sP = [&](int j) -> E& { return sx[(2 * j) * T + threadIdx.x]; };
@@ -83,6 +85,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       txslot_init(tx_e);
       txslot_init(tx_ssq);
       txslot_init(tx_dot);
+      txslot_init(tx_f1);
+      txslot_init(tx_f2);
     }
     txred_publish();
   }
@@ -150,124 +154,199 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     }
   }
 
-  // @phase spade:norms
-  // ---- spade: E = floor(lg max |component|) per column (high words)
-  uint32_t hp = 0, hq = 0;
+  // ---- the norms (spade) and the dot (club) of the pair, two ways with the
+  // same bits.  Fast (DESIGN.md 4.6 applied to the step): every component
+  // scaled by one 2^-c (c: floor(lg M-tilde) in the driver, F(m) - 1 for the
+  // public step), the sums of squares and the dot accumulated in ONE pass and
+  // reduced in one round of two pairs; valid while every nonzero scaled value
+  // is in [2^-400, 2^16] (checked per lane; a failing lane turns its SSQ into
+  // NaN, so the whole pair sees it and takes the exact path).  Exact: the
+  // per-column exponent max, then the SSQ of x 2^-E, then the prescaled dot
+  // (three rounds).
+  double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0, zr = 0.0, zi = 0.0;
+  bool zero_col = false, fastp = false;
+  // @phase spade+club:fast
+  if (P.fast) {
+    const int c = P.Mt ? ilogb_bits(mt_cur) + sn : P.Fm - 1;
+    if (c >= 600 && c <= 1023) {  // cluster-uniform
+      const double a = pow2i(-c);
+      double sp = 0.0, sq = 0.0, ar = 0.0, ai = 0.0;
+      uint32_t lmin = ~0u, lmax = 0;
 #pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    hp = hi_max(xp[j], hp);
-    hq = hi_max(xq[j], hq);
-  }
+      for (int j = 0; j < NR; ++j) {
+        const E yp = scale1(xp[j], a), yq = scale1(xq[j], a);
+        sp = ssq_acc(yp, sp);
+        sq = ssq_acc(yq, sq);
+        dot_acc(yq, yp, ar, ai);
+        lmin = lo_hi_min(yp, lo_hi_min(yq, lmin));
+        lmax = hi_max(yp, hi_max(yq, lmax));
+      }
 #pragma unroll 2
-  for (int j = 0; j < NS; ++j) {
-    hp = hi_max(sP(j), hp);
-    hq = hi_max(sQ(j), hq);
-  }
-  int Ep, Eq;
-  if (hp >= 0x00100000u) {
-    Ep = static_cast<int>(hp >> 20) - 1023;
-  } else {  // largest component subnormal or zero: exact from the bit patterns
-    uint64_t mb = 0;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) mb = absmax_bits(xp[j], mb);
-#pragma unroll 2
-    for (int j = 0; j < NS; ++j) mb = absmax_bits(sP(j), mb);
-    Ep = ilogb_or_min(mb);
-  }
-  if (hq >= 0x00100000u) {
-    Eq = static_cast<int>(hq >> 20) - 1023;
-  } else {
-    uint64_t mb = 0;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) mb = absmax_bits(xq[j], mb);
-#pragma unroll 2
-    for (int j = 0; j < NS; ++j) mb = absmax_bits(sQ(j), mb);
-    Eq = ilogb_or_min(mb);
-  }
-  if constexpr (CL > 1) tree_max2i_tx<T, CL>(Ep, Eq, rs_e, tx_e);
-  else tree_max2i<T, 1>(Ep, Eq, rs_e);
-  // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform; the
-  // two-multiply case 2^-E < 2^-1074 is a uniform branch).  Zero padding adds
-  // exact zeros to a non-negative sum.
-  double sp = 0.0, sq = 0.0;
-  if (Ep != kIntMin) {
-    if (-Ep > 1023) {
-      const double a = 0x1p1023, b = pow2i(-Ep - 1023);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) sp = ssq_acc(scale2(xp[j], a, b), sp);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j) sp = ssq_acc(scale2(sP(j), a, b), sp);
-    } else {
-      // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
-      // field only; a subnormal 2^-E (outside it) the general construction
-      const double a = -Ep >= -1022 ? pow2i(-Ep) : pow2_any(-Ep);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) sp = ssq_acc(scale1(xp[j], a), sp);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j) sp = ssq_acc(scale1(sP(j), a), sp);
+      for (int j = 0; j < NS; ++j) {
+        const E yp = scale1(sP(j), a), yq = scale1(sQ(j), a);
+        sp = ssq_acc(yp, sp);
+        sq = ssq_acc(yq, sq);
+        dot_acc(yq, yp, ar, ai);
+        lmin = lo_hi_min(yp, lo_hi_min(yq, lmin));
+        lmax = hi_max(yp, hi_max(yq, lmax));
+      }
+      if (lmin < kFastLo - 1u || lmax >= kFastHi) sp = __longlong_as_double(0x7ff8000000000000ll);
+      if constexpr (CL > 1) {
+        tree_sum2_tx<T, CL>(sp, sq, rs_f1, tx_f1);
+        tree_sum2_tx<T, CL>(ar, ai, rs_f2, tx_f2);
+      } else {
+        tree_sum2<T, 1>(sp, sq, rs_f1);
+        tree_sum2<T, 1>(ar, ai, rs_f2);
+      }
+      if (!isnan(sp)) {  // uniform: every lane holds the totals
+        fastp = true;
+        // R#14 with E := c (the SSQ of x 2^-c carries 2^(2E - 2c) exactly)
+        int iep = kIntMin, ieq = kIntMin;
+        double gp = 1.0, gq = 1.0;
+        if (sp > 0.0) {
+          eg_from_ssq_c(c, sp, iep, gp);
+          ep = static_cast<double>(iep);
+          fp = sqrt_plain(gp);
+        }
+        if (sq > 0.0) {
+          eg_from_ssq_c(c, sq, ieq, gq);
+          eq = static_cast<double>(ieq);
+          fq = sqrt_plain(gq);
+        }
+        zero_col = !(sp > 0.0) || !(sq > 0.0);  // R#19
+        if (!zero_col) {  // the dot of x 2^-c carries 2^(2c - e_q - e_p) exactly
+          const double f2 = pow2i(2 * c - iep - ieq);
+          const Rcp d = rcp_plain(fq * fp);  // fl(f_q f_p) in [1, 4)
+          zr = dot_div(ar * f2, d, kFull);
+          zi = CPLX ? dot_div(ai * f2, d, kFull) : 0.0;
+        }
+        if (lead) {
+          P.col_e[p] = ep;
+          P.col_f[p] = fp;
+          P.col_e[q] = eq;
+          P.col_f[q] = fq;
+        }
+      }
     }
   }
-  if (Eq != kIntMin) {
-    if (-Eq > 1023) {
-      const double a = 0x1p1023, b = pow2i(-Eq - 1023);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) sq = ssq_acc(scale2(xq[j], a, b), sq);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j) sq = ssq_acc(scale2(sQ(j), a, b), sq);
-    } else {
-      // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
-      // field only; a subnormal 2^-E (outside it) the general construction
-      const double a = -Eq >= -1022 ? pow2i(-Eq) : pow2_any(-Eq);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) sq = ssq_acc(scale1(xq[j], a), sq);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j) sq = ssq_acc(scale1(sQ(j), a), sq);
+  if (!fastp) {
+    // @phase spade:norms
+    // ---- spade: E = floor(lg max |component|) per column (high words)
+    uint32_t hp = 0, hq = 0;
+  #pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      hp = hi_max(xp[j], hp);
+      hq = hi_max(xq[j], hq);
     }
-  }
-  if constexpr (CL > 1) tree_sum2_tx<T, CL>(sp, sq, rs_ssq, tx_ssq);
-  else tree_sum2<T, 1>(sp, sq, rs_ssq);
-  double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0;
-  if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
-  if (Eq != kIntMin) ef_from_ssq(Eq, sq, eq, fq);
-  if (lead) {
-    P.col_e[p] = ep;
-    P.col_f[p] = fp;
-    P.col_e[q] = eq;
-    P.col_f[q] = fq;
-  }
+  #pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      hp = hi_max(sP(j), hp);
+      hq = hi_max(sQ(j), hq);
+    }
+    int Ep, Eq;
+    if (hp >= 0x00100000u) {
+      Ep = static_cast<int>(hp >> 20) - 1023;
+    } else {  // largest component subnormal or zero: exact from the bit patterns
+      uint64_t mb = 0;
+  #pragma unroll
+      for (int j = 0; j < NR; ++j) mb = absmax_bits(xp[j], mb);
+  #pragma unroll 2
+      for (int j = 0; j < NS; ++j) mb = absmax_bits(sP(j), mb);
+      Ep = ilogb_or_min(mb);
+    }
+    if (hq >= 0x00100000u) {
+      Eq = static_cast<int>(hq >> 20) - 1023;
+    } else {
+      uint64_t mb = 0;
+  #pragma unroll
+      for (int j = 0; j < NR; ++j) mb = absmax_bits(xq[j], mb);
+  #pragma unroll 2
+      for (int j = 0; j < NS; ++j) mb = absmax_bits(sQ(j), mb);
+      Eq = ilogb_or_min(mb);
+    }
+    if constexpr (CL > 1) tree_max2i_tx<T, CL>(Ep, Eq, rs_e, tx_e);
+    else tree_max2i<T, 1>(Ep, Eq, rs_e);
+    // ---- spade: SSQ of x 2^-E in the lane order of R (E is CTA-uniform; the
+    // two-multiply case 2^-E < 2^-1074 is a uniform branch).  Zero padding adds
+    // exact zeros to a non-negative sum.
+    double sp = 0.0, sq = 0.0;
+    if (Ep != kIntMin) {
+      if (-Ep > 1023) {
+        const double a = 0x1p1023, b = pow2i(-Ep - 1023);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j) sp = ssq_acc(scale2(xp[j], a, b), sp);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j) sp = ssq_acc(scale2(sP(j), a, b), sp);
+      } else {
+        // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
+        // field only; a subnormal 2^-E (outside it) the general construction
+        const double a = -Ep >= -1022 ? pow2i(-Ep) : pow2_any(-Ep);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j) sp = ssq_acc(scale1(xp[j], a), sp);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j) sp = ssq_acc(scale1(sP(j), a), sp);
+      }
+    }
+    if (Eq != kIntMin) {
+      if (-Eq > 1023) {
+        const double a = 0x1p1023, b = pow2i(-Eq - 1023);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j) sq = ssq_acc(scale2(xq[j], a, b), sq);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j) sq = ssq_acc(scale2(sQ(j), a, b), sq);
+      } else {
+        // 2^-E normal (the step's precondition keeps max|x| < 2^1022): exponent
+        // field only; a subnormal 2^-E (outside it) the general construction
+        const double a = -Eq >= -1022 ? pow2i(-Eq) : pow2_any(-Eq);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j) sq = ssq_acc(scale1(xq[j], a), sq);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j) sq = ssq_acc(scale1(sQ(j), a), sq);
+      }
+    }
+    if constexpr (CL > 1) tree_sum2_tx<T, CL>(sp, sq, rs_ssq, tx_ssq);
+    else tree_sum2<T, 1>(sp, sq, rs_ssq);
+    if (Ep != kIntMin) ef_from_ssq(Ep, sp, ep, fp);
+    if (Eq != kIntMin) ef_from_ssq(Eq, sq, eq, fq);
+    if (lead) {
+      P.col_e[p] = ep;
+      P.col_f[p] = fp;
+      P.col_e[q] = eq;
+      P.col_f[q] = fq;
+    }
 
-  // @phase club:dot
-  // ---- club: a21' = (g_q 2^-e_q)^* (g_p 2^-e_p) / fl(f_q f_p)  (Alg 3.1)
-  double zr = 0.0, zi = 0.0;
-  const bool zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19 (cluster-uniform)
-  if (!zero_col) {
-    const int iq = static_cast<int>(eq), ip = static_cast<int>(ep);
-    double ar = 0.0, ai = 0.0;
-    if (-iq > 1023 || -ip > 1023) {
-      const Pow2 fQ(-iq), fP(-ip);
-#pragma unroll
-      for (int j = 0; j < NR; ++j)
-        dot_acc(scale2(xq[j], fQ.a, fQ.b), scale2(xp[j], fP.a, fP.b), ar, ai);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j)
-        dot_acc(scale2(sQ(j), fQ.a, fQ.b), scale2(sP(j), fP.a, fP.b), ar, ai);
-    } else {
-      const double aq = pow2_any(-iq), ap = pow2_any(-ip);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
-#pragma unroll 2
-      for (int j = 0; j < NS; ++j) dot_acc(scale1(sQ(j), aq), scale1(sP(j), ap), ar, ai);
+    // @phase club:dot
+    // ---- club: a21' = (g_q 2^-e_q)^* (g_p 2^-e_p) / fl(f_q f_p)  (Alg 3.1)
+    zero_col = (Ep == kIntMin) || (Eq == kIntMin);  // R#19 (cluster-uniform)
+    if (!zero_col) {
+      const int iq = static_cast<int>(eq), ip = static_cast<int>(ep);
+      double ar = 0.0, ai = 0.0;
+      if (-iq > 1023 || -ip > 1023) {
+        const Pow2 fQ(-iq), fP(-ip);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j)
+          dot_acc(scale2(xq[j], fQ.a, fQ.b), scale2(xp[j], fP.a, fP.b), ar, ai);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j)
+          dot_acc(scale2(sQ(j), fQ.a, fQ.b), scale2(sP(j), fP.a, fP.b), ar, ai);
+      } else {
+        const double aq = pow2_any(-iq), ap = pow2_any(-ip);
+  #pragma unroll
+        for (int j = 0; j < NR; ++j) dot_acc(scale1(xq[j], aq), scale1(xp[j], ap), ar, ai);
+  #pragma unroll 2
+        for (int j = 0; j < NS; ++j) dot_acc(scale1(sQ(j), aq), scale1(sP(j), ap), ar, ai);
+      }
+      if constexpr (CL > 1) tree_sum2_tx<T, CL>(ar, ai, rs_dot, tx_dot);
+      else tree_sum2<T, 1>(ar, ai, rs_dot);
+      const Rcp d = rcp_plain(fq * fp);  // fl(f_q f_p) in [1, 4)
+      zr = dot_div(ar, d, kFull);
+      zi = CPLX ? dot_div(ai, d, kFull) : 0.0;
     }
-    if constexpr (CL > 1) tree_sum2_tx<T, CL>(ar, ai, rs_dot, tx_dot);
-    else tree_sum2<T, 1>(ar, ai, rs_dot);
-    const Rcp d = rcp_plain(fq * fp);  // fl(f_q f_p) in [1, 4)
-    zr = dot_div(ar, d, kFull);
-    zi = CPLX ? dot_div(ai, d, kFull) : 0.0;
   }
   // the last cross-CTA round is done: arrive now, wait at exit (no CTA leaves
   // while a peer's push into its shared memory could still be in flight)
   if constexpr (CL > 1) {
-    if (!zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (fastp || !zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   }
   // @phase heart:test+V-prefetch
   // ---- heart: transform iff upsilon <= |a21'| (Alg 3.2)
@@ -401,7 +480,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     P.s_slots[(P.slot + 1) % 3] = P.s_slots[P.slot] + sn;
   }
   if constexpr (CL > 1) {
-    if (zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (!fastp && zero_col) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
   }
 }
@@ -602,6 +681,23 @@ cudaError_t launch_colnorm(bool cplx, int64_t m, int64_t n, const double* G, int
 
 bool step_supported(bool cplx, int64_t m) { return pick_geo(cplx, m).T != 0; }
 
+// JSVD_STEP_FAST=0: the step kernel's exact norms + dot only (A/B runs; the
+// same bits either way -- the GPU tests compare both)
+bool step_fast_enabled() {
+  const char* e = getenv("JSVD_STEP_FAST");
+  return !e || atoi(e) != 0;
+}
+
+// floor(lg(omega/(2m))) (real) / floor(lg(omega/(4 m sqrt2))) (complex) (R#28):
+// the public step's scale 2^(F(m)-1) bounds a matrix pre-scaled as jsvd_gesvj does
+static int Fm_step(bool cplx, int64_t m) {
+  int k = 0;
+  while ((m >> (k + 1)) > 0) ++k;
+  if (!cplx) return 1022 - k;
+  const unsigned __int128 mm = static_cast<unsigned __int128>(m) * static_cast<unsigned __int128>(m);
+  return 1021 - k - (mm >= (static_cast<unsigned __int128>(1) << (2 * k + 1)) ? 1 : 0);
+}
+
 __global__ void strategy_kernel(int64_t n, int64_t B, int64_t step, int32_t* pairs) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l < n / 2) {
@@ -676,6 +772,8 @@ extern "C" jsvd_status jsvd_sweep_step(jsvd_dtype dt, int64_t m, int64_t n, doub
   P.col_f = col_f;
   P.t_dev = reinterpret_cast<unsigned long long*>(t_dev);
   P.mmax = reinterpret_cast<unsigned long long*>(mmax_dev);
+  P.fast = step_fast_enabled() ? 1 : 0;
+  P.Fm = Fm_step(cplx, m);
   cudaError_t e = launch_step(cplx, npairs, P, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? JSVD_OK : JSVD_ECUDA;
 }

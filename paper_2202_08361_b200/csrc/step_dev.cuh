@@ -333,6 +333,32 @@ __device__ __forceinline__ void ef_from_ssq(int E, double ssq, double& e, double
   e = static_cast<double>(E + k / 2);
 }
 
+// ---- the scaled domain of DESIGN.md 4.6 (batched kernels, step kernel):
+// every nonzero scaled value in [2^-400, 2^16], i.e. a high word (sign
+// masked) of at least kFastLo and below kFastHi.  lo_hi_min folds hi(|x|) - 1
+// into a running minimum (0 maps to 0xffffffff and passes).
+constexpr uint32_t kFastLo = static_cast<uint32_t>(1023 - 400) << 20;
+constexpr uint32_t kFastHi = static_cast<uint32_t>(1023 + 16) << 20;
+__device__ __forceinline__ uint32_t lo_hi_min(double x, uint32_t m) {
+  return min(m, (hi32(x) & 0x7fffffffu) - 1u);
+}
+__device__ __forceinline__ uint32_t lo_hi_min(double2 x, uint32_t m) {
+  return min(m, min((hi32(x.x) & 0x7fffffffu) - 1u, (hi32(x.y) & 0x7fffffffu) - 1u));
+}
+// e = E + k/2 and g = SSQ 2^-k (k even) from a positive normal sum of squares
+// (R#14), E the scale exponent the squared values carry
+__device__ __forceinline__ void eg_from_ssq_c(int E, double ssq, int& e, double& g) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(ssq));
+  int k = static_cast<int>(b >> 52) - 1023;
+  g = __longlong_as_double(static_cast<long long>((b & 0x000fffffffffffffull) |
+                                                  0x3ff0000000000000ull));
+  if (k & 1) {
+    g = g * 2.0;
+    k -= 1;
+  }
+  e = E + k / 2;
+}
+
 // fold one element into the SSQ accumulator (fma(y,y,.) re then im)
 __device__ __forceinline__ double ssq_acc(double y, double acc) { return fma(y, y, acc); }
 __device__ __forceinline__ double ssq_acc(double2 y, double acc) {

@@ -13,6 +13,7 @@ struct StepParams {
   const int32_t* pairs;  // explicit pairs, or nullptr -> strategy (B, step)
   int64_t B, step;
   int dist_nr, dist_rank;  // dist_nr > 0: this rank's local pairs of the sharded ordering
+  int fast;                // the scaled single-pass norms + dot, with fallback
   double tol;
   double* col_e;
   double* col_f;
