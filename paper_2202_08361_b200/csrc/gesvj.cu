@@ -173,6 +173,24 @@ __global__ void normalize_kernel(int64_t rows, double* G, int64_t ld, const doub
     G[j * ld + i] = divide(sc(G[j * ld + i]), d);
 }
 
+// a rank's own block moves of one exchange in one launch: block k of the
+// table goes from slot src[k] to slot dst[k] of G and of V (16-byte words)
+struct LocalMoves {
+  int n;
+  int src[32], dst[32];
+};
+__global__ void local_moves_kernel(const double2* __restrict__ G, double2* __restrict__ G2,
+                                   int64_t gw, const double2* __restrict__ V,
+                                   double2* __restrict__ V2, int64_t vw, LocalMoves mv) {
+  const int k = blockIdx.y;
+  const int64_t s = mv.src[k], d = mv.dst[k];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < gw + vw;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < gw) G2[d * gw + i] = G[s * gw + i];
+    else V2[d * vw + (i - gw)] = V[s * vw + (i - gw)];
+  }
+}
+
 static int ilog2_floor(int64_t m) {
   int k = 0;
   while ((m >> (k + 1)) > 0) ++k;
@@ -252,6 +270,9 @@ class Comm {
 
   // in place over one 64-bit word on the device: op 0 max (u64), 1 sum (i64)
   jsvd_status allreduce(void* dev, int op) {
+    // one rank: the local value is the global one (JSVD_DIST_SELF_P2P still
+    // runs the NCCL collective, to exercise it on one GPU)
+    if (d_->nranks == 1 && !(d_->flags & JSVD_DIST_SELF_P2P)) return JSVD_OK;
     if (nccl()) {
       ncclResult_t r = ncclAllReduce(dev, dev, 1, op == 0 ? ncclUint64 : ncclInt64,
                                      op == 0 ? ncclMax : ncclSum,
@@ -271,6 +292,7 @@ class Comm {
 
   // recv (device, nranks * bytes) = every rank's send (device, bytes)
   jsvd_status allgather(const void* send, void* recv, size_t bytes, int nranks) {
+    if (nranks == 1 && !(d_->flags & JSVD_DIST_SELF_P2P) && send == recv) return JSVD_OK;
     if (nccl()) {
       ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8,
                                      static_cast<ncclComm_t>(d_->nccl_comm), st_);
@@ -524,6 +546,7 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
   auto exchange = [&]() -> jsvd_status {
     const int nslots = static_cast<int>(nl / b);
     std::vector<std::pair<int, Comm::Op>> sends, recvs;
+    LocalMoves mv{};
     for (int sl = 0; sl < nslots; ++sl) {  // outgoing
       const int pos = dist_slot_position(nblocks, nr, dist->rank, sl);
       const int dpos = pos == 0 ? 0 : (pos >= 2 ? pos - 1 : nblocks - 1);
@@ -531,11 +554,10 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
       dist_owner(nblocks, nr, dpos, dr, ds);
       char* gs = reinterpret_cast<char*>(Gcur) + sl * gblk;
       char* vs = reinterpret_cast<char*>(Vcur) + sl * vblk;
-      if (dr == dist->rank && !self_p2p) {
-        CK(cudaMemcpyAsync(reinterpret_cast<char*>(Galt) + ds * gblk, gs, gblk,
-                           cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpyAsync(reinterpret_cast<char*>(Valt) + ds * vblk, vs, vblk,
-                           cudaMemcpyDeviceToDevice, st));
+      if (dr == dist->rank && !self_p2p) {  // one kernel for all of them (below)
+        mv.src[mv.n] = sl;
+        mv.dst[mv.n] = ds;
+        ++mv.n;
       } else {
         sends.push_back({2 * pos, {dr, 0, gs, gblk}});
         sends.push_back({2 * pos + 1, {dr, 0, vs, vblk}});
@@ -558,6 +580,15 @@ extern "C" jsvd_status jsvd_gesvj(jsvd_dtype dt, int64_t m, int64_t n, double* A
     std::vector<Comm::Op> ops;
     for (const auto& o : sends) ops.push_back(o.second);
     for (const auto& o : recvs) ops.push_back(o.second);
+    if (mv.n) {
+      const int64_t gw = static_cast<int64_t>(gblk / 16), vw = static_cast<int64_t>(vblk / 16);
+      const unsigned bx = static_cast<unsigned>(std::min<int64_t>((gw + vw + 255) / 256, 512));
+      local_moves_kernel<<<dim3(bx, mv.n), 256, 0, st>>>(
+          reinterpret_cast<const double2*>(Gcur), reinterpret_cast<double2*>(Galt), gw,
+          reinterpret_cast<const double2*>(Vcur), reinterpret_cast<double2*>(Valt), vw, mv);
+      note_launch();
+      CK(cudaGetLastError());
+    }
     CS(comm.p2p(ops));
     std::swap(Gcur, Galt);
     std::swap(Vcur, Valt);
