@@ -158,9 +158,10 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   // same bits.  Fast (DESIGN.md 4.6 applied to the step): every component
   // scaled by one 2^-c (c: floor(lg M-tilde) in the driver, F(m) - 1 for the
   // public step), the sums of squares and the dot accumulated in ONE pass and
-  // reduced in one round of two pairs; valid while every nonzero scaled value
-  // is in [2^-400, 2^16] (checked per lane; a failing lane turns its SSQ into
-  // NaN, so the whole pair sees it and takes the exact path).  Exact: the
+  // reduced in one round of two pairs; valid while every nonzero value is in
+  // [2^(c-400), 2^(c+16)) (checked per lane on the unscaled values; a failing
+  // lane turns its SSQ into NaN, so the whole pair sees it and takes the
+  // exact path).  Exact: the
   // per-column exponent max, then the SSQ of x 2^-E, then the prescaled dot
   // (three rounds).
   double ep = -INFINITY, fp = 1.0, eq = -INFINITY, fq = 1.0, zr = 0.0, zi = 0.0;
@@ -171,6 +172,8 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
     if (c >= 600 && c <= 1023) {  // cluster-uniform
       const double a = pow2i(-c);
       double sp = 0.0, sq = 0.0, ar = 0.0, ai = 0.0;
+      // the domain check on the UNscaled values (a scaled value could have
+      // underflowed): nonzero |x| in [2^(c-400), 2^(c+16))
       uint32_t lmin = ~0u, lmax = 0;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
@@ -178,19 +181,22 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
         sp = ssq_acc(yp, sp);
         sq = ssq_acc(yq, sq);
         dot_acc(yq, yp, ar, ai);
-        lmin = lo_hi_min(yp, lo_hi_min(yq, lmin));
-        lmax = hi_max(yp, hi_max(yq, lmax));
+        lmin = lo_hi_min(xp[j], lo_hi_min(xq[j], lmin));
+        lmax = hi_max(xp[j], hi_max(xq[j], lmax));
       }
 #pragma unroll 2
       for (int j = 0; j < NS; ++j) {
-        const E yp = scale1(sP(j), a), yq = scale1(sQ(j), a);
+        const E xpj = sP(j), xqj = sQ(j);
+        const E yp = scale1(xpj, a), yq = scale1(xqj, a);
         sp = ssq_acc(yp, sp);
         sq = ssq_acc(yq, sq);
         dot_acc(yq, yp, ar, ai);
-        lmin = lo_hi_min(yp, lo_hi_min(yq, lmin));
-        lmax = hi_max(yp, hi_max(yq, lmax));
+        lmin = lo_hi_min(xpj, lo_hi_min(xqj, lmin));
+        lmax = hi_max(xpj, hi_max(xqj, lmax));
       }
-      if (lmin < kFastLo - 1u || lmax >= kFastHi) sp = __longlong_as_double(0x7ff8000000000000ll);
+      const uint32_t lo = static_cast<uint32_t>(c - 400 + 1023) << 20;
+      const uint32_t hi = static_cast<uint32_t>(min(c + 16 + 1023, 2047)) << 20;
+      if (lmin < lo - 1u || lmax >= hi) sp = __longlong_as_double(0x7ff8000000000000ll);
       if constexpr (CL > 1) {
         tree_sum2_tx<T, CL>(sp, sq, rs_f1, tx_f1);
         tree_sum2_tx<T, CL>(ar, ai, rs_f2, tx_f2);
