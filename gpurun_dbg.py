@@ -1,20 +1,22 @@
-import numpy as np, torch, sys
+import numpy as np, torch, sys, os
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
 import oracle as O, paper_2202_08361_b200 as J
-from test_gpu_svd import _scaled_input, rspec, colmajor_gpu, to_np
-for cplx in (False, True):
-    m = 64; n = 12
-    rng = np.random.default_rng(m + 7 * cplx)
-    A = _scaled_input(rng, m, n, cplx)
-    V = np.asfortranarray(np.eye(n, dtype=A.dtype) + 0.0)
-    R = rspec(J, cplx, m)
-    G_ref, V_ref = A.copy(order="F"), V.copy(order="F")
-    g, v = colmajor_gpu(A), colmajor_gpu(V)
-    pairs = O.strategy_pairs(n, n, 0)
-    ref = O.step(G_ref, V_ref, pairs, R)
-    out = J.sweep_step(g, v, torch.from_numpy(pairs.astype(np.int32)).cuda())
-    torch.cuda.synchronize()
-    ce, cf = out["col_e"].cpu().numpy(), out["col_f"].cpu().numpy()
-    print("cplx", cplx, "pairs", pairs.tolist())
-    for j in range(n):
-        print(j, ce[j], ref["col_e"][j], cf[j], ref["col_f"][j], "OK" if (ce[j] == ref["col_e"][j] and cf[j] == ref["col_f"][j]) else "DIFF")
+from test_gpu_dist import _case, _rspec
+m, n = 96, 64
+for cplx in (False,):
+    A = _case(cplx, m, n, seed=3)
+    K = 1022
+    adj = K + 1 - O.Fm(cplx, m)
+    ref = O.gesvj(A, _rspec(cplx, m), B=16, max_sweeps=30, s0_adjust=adj)
+    for B in (16, 64):
+        refB = O.gesvj(A, _rspec(cplx, m), B=B, max_sweeps=30, s0_adjust=adj)
+        g = torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T
+        out = J.gesvj(g, nblocks=B, max_sweeps=30, s0_adjust=adj)
+        print("B", B, "gpu tps", out["tps"][:6], "scale", out["scale"], "sweeps", out["sweeps"])
+        print("B", B, "orc tps", list(refB["tps"][:6]), "scale", refB["scale"], "sweeps", refB["sweeps"])
+    # no adjust
+    for B in (16,):
+        refB = O.gesvj(A, _rspec(cplx, m), B=B, max_sweeps=30)
+        g = torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T
+        out = J.gesvj(g, nblocks=B, max_sweeps=30)
+        print("noadj B", B, out["tps"][:6], list(refB["tps"][:6]))

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
   // @phase spade+club:fast
   if (P.fast) {
     const int c = P.Mt ? ilogb_bits(mt_cur) + sn : P.Fm - 1;
-    if (c >= 600 && c <= 1023) {  // cluster-uniform
+    if (c >= 600 && c <= 1022) {  // cluster-uniform (2^-c normal)
       const double a = pow2i(-c);
       double sp = 0.0, sq = 0.0, ar = 0.0, ai = 0.0;
       // the domain check on the UNscaled values (a scaled value could have
