@@ -457,3 +457,41 @@ def test_gesvj_batched_fast_mode_is_invisible(J, monkeypatch, cplx, kind):
         V = o["V"].transpose(1, 2).contiguous().cpu().numpy().transpose(0, 2, 1)
         assert bits_equal(U[ok], ref["U"][ok]) and bits_equal(V[ok], ref["V"][ok]), fast
         assert bits_equal(o["sigma"].cpu().numpy()[ok], ref["sigma"][ok]), fast
+
+
+@pytest.mark.parametrize("fast", ["0", "1"])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_step_both_paths_bitwise(J, monkeypatch, fast, cplx):
+    # the step kernel's scaled single-pass norms + dot and its
+    # exact three-round path (JSVD_STEP_FAST=0) give the oracle's bits: sweep
+    # steps with zero, subnormal, tiny (2^-1000) and huge (2^600) columns at
+    # the cluster geometries, and full SVDs with block ordering whose scale
+    # sits at the top of the range (s0_adjust: floor(lg M~) = K, then K + 1)
+    monkeypatch.setenv("JSVD_STEP_FAST", fast)
+    for m in (300, 4096 if not cplx else 2049, 20001):
+        n = 12
+        rng = np.random.default_rng(m + 3 * cplx + 11)
+        A = _scaled_input(rng, m, n, cplx)
+        V = np.asfortranarray(np.eye(n, dtype=A.dtype) + 0.0)
+        R = rspec(J, cplx, m)
+        G_ref, V_ref = A.copy(order="F"), V.copy(order="F")
+        g, v = colmajor_gpu(A), colmajor_gpu(V)
+        for k in range(3):
+            pairs = O.strategy_pairs(n, n, k)
+            ref = O.step(G_ref, V_ref, pairs, R)
+            out = J.sweep_step(g, v, torch.from_numpy(pairs.astype(np.int32)).cuda())
+            torch.cuda.synchronize()
+            assert bits_equal(to_np(g), G_ref) and bits_equal(to_np(v), V_ref), (m, k)
+            assert bits_equal(out["col_e"].cpu().numpy(), ref["col_e"]), (m, k)
+            assert bits_equal(out["col_f"].cpu().numpy(), ref["col_f"]), (m, k)
+    K = 1020 if cplx else 1022
+    m, n = 96, 64
+    rng = np.random.default_rng(5 + cplx)
+    A = rng.standard_normal((m, n)) + (1j * rng.standard_normal((m, n)) if cplx else 0)
+    R = O.RSpec.make(256, 1, [16, 8, 4, 2, 1, 128, 64, 32])
+    for adj in (0, K + 1 - O.Fm(cplx, m)):
+        ref = O.gesvj(A, R, B=16, max_sweeps=30, s0_adjust=adj)
+        out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), nblocks=16, max_sweeps=30, s0_adjust=adj)
+        assert list(out["tps"]) == list(ref["tps"]) and out["scale"] == ref["scale"], adj
+        assert bits_equal(to_np(out["U"]), ref["U"]) and bits_equal(to_np(out["V"]), ref["V"]), adj
+        assert bits_equal(out["sigma"].cpu().numpy(), ref["sigma"]), adj
