@@ -997,7 +997,7 @@ def run_jsvd(args):
             "cpu_baseline": cpu,
         }
         line.update(extra)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 
@@ -1097,7 +1097,7 @@ def run_reference(args):
                          "kind": "oracle", "sample": wl.what},
         "e2e": {"value": v, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 class ReferenceWorkload:
@@ -1176,7 +1176,26 @@ class ReferenceWorkload:
             self.what = "16 matrices of the batch per step"
 
 
+def _claim_stdout():
+    """stdout carries exactly the JSON line: everything else written to fd 1
+    by libraries (NCCL's version banner at communicator creation, ...) goes
+    to stderr; returns the stream the JSON line is printed on."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
+
+JSON_OUT = None
+
+
+def emit(line):
+    print(json.dumps(line), file=JSON_OUT or sys.stdout, flush=True)
+
+
 def main():
+    global JSON_OUT
+    JSON_OUT = _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)

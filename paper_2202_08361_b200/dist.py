@@ -50,6 +50,27 @@ def gesvj_sharded(A_local, n, nblocks, dist, **kw):
     return J.gesvj(A_local, nblocks=nblocks, dist=dist, n=n, **kw)
 
 
+class _StdoutToStderr:
+    """fd-level redirect of stdout to stderr (NCCL may print its version banner
+    on stdout at communicator creation; stdout stays clean for callers that
+    print machine-readable output, such as bench.py's JSON line)."""
+
+    def __enter__(self):
+        import os
+        import sys
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        import os
+        import sys
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+
+
 class NcclDist:
     """The library's NCCL communicator for this process's rank of `group`
     (torch.distributed, any backend; only the unique id travels through it).
@@ -61,7 +82,8 @@ class NcclDist:
         obj = [J.nccl_unique_id() if rank == 0 else None]
         src = dist.get_global_rank(group, 0) if group is not None else 0
         dist.broadcast_object_list(obj, src=src, group=group)
-        self.comm = J.nccl_comm_init(world, obj[0], rank)
+        with _StdoutToStderr():
+            self.comm = J.nccl_comm_init(world, obj[0], rank)
         self.dist = J.Dist(self.comm, rank, world, None, flags)
 
     @classmethod
@@ -69,7 +91,8 @@ class NcclDist:
         """A world of one rank (no torch.distributed needed): with
         DIST_SELF_P2P every block move goes through NCCL send/recv to self."""
         self = cls.__new__(cls)
-        self.comm = J.nccl_comm_init(1, J.nccl_unique_id(), 0)
+        with _StdoutToStderr():
+            self.comm = J.nccl_comm_init(1, J.nccl_unique_id(), 0)
         self.dist = J.Dist(self.comm, 0, 1, None, flags)
         return self
 

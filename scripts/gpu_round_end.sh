@@ -10,6 +10,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $
 timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 400 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; echo "rc=$?" >> $OUT/bench_default.err
+timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench_default_20.json 2> $OUT/bench_default_20.err; echo "rc=$?" >> $OUT/bench_default_20.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "rc=$?" >> $OUT/bench_reference.err
 for w in ${WORKLOADS:-evd_r64 evd_c32 step_r64 step_c64 batched_c64 gesvj_r64 dist_c64 norm_c64 gs_r64}; do
   timeout 1200 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err; echo "rc=$?" >> $OUT/bench_$w.err
@@ -20,7 +21,7 @@ $B --steps 20 > $OUT/plain_launch.log 2>&1 && \
   $B --steps 20 > $OUT/ncu_launch.log 2>&1
 for w in ${KW:-evd_c64 evd_r64 evd_c32 step_r64 step_c64 batched_c64 norm_c64 gs_r64}; do
   case $w in evd_c64) K=evd2_vec2;; evd_r64) K=evd2_scalar;; evd_c32) K=evd2f_;; step_*) K=step_kernel;;
-    batched_c64) K=batched_svd;; norm_c64) K=norm_ef;; gs_r64) K=dgsscl;; esac
+    batched_c64) K=batched_fast;; norm_c64) K=norm_ef;; gs_r64) K=dgsscl;; esac
   S=5; [ $w = batched_c64 ] && S=3
   $B --workload $w --steps 4 > $OUT/plain_$w.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
