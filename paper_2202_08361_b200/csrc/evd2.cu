@@ -5,23 +5,14 @@
 // every SoA input stream with one 16-byte LDG.128 (coalesced, 512 B per warp
 // per stream), runs the EVD in registers, and stores every output stream with
 // one 16-byte STG.128; the permutation words are assembled from two
-// warp ballots.  No shared memory, no synchronisation.  Grid: one 256-thread
-// CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110 waves at 8 CTAs/SM).
+// shuffles and two warp ballots.  No shared memory, no synchronisation.
+// Grid: one 256-thread CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110
+// waves at 8 CTAs/SM).
 #include "jsvd_dev.cuh"
 
 #include "jsvd_host.h"
 
 namespace jsvd {
-
-// spread the low 16 bits of x to the even bit positions
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-  x &= 0xffffu;
-  x = (x | (x << 8)) & 0x00ff00ffu;
-  x = (x | (x << 4)) & 0x0f0f0f0fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
-}
 
 // streaming loads of one chunk (512 matrices per CTA, 2 per thread); lanes
 // past r read zeros (every lane runs the EVD so the rare-case votes can use
@@ -50,7 +41,7 @@ struct Chunk2 {
 };
 
 // one chunk: 512 consecutive matrices, 2 per thread (LDG.128 / STG.128 of
-// every SoA stream); the permutation words from two warp ballots
+// every SoA stream); the permutation words from two shuffles + two ballots
 template <bool CPLX, bool TAN, bool NOBACK>
 __device__ __forceinline__ void evd2_chunk(
     int64_t c, int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
@@ -80,15 +71,17 @@ __device__ __forceinline__ void evd2_chunk(
     if (zeta) zeta[l0] = e0.zeta;
   }
   if (perm) {  // warp covers matrices [64w, 64w+64): words 2w, 2w+1
-    const uint32_t b0 = __ballot_sync(0xffffffffu, p0);
-    const uint32_t b1 = __ballot_sync(0xffffffffu, p1);
+    // bit j of word 2w + h is matrix 64w + 32h + j, held by lane 16h + j/2 as
+    // its EVD j&1: fetch that lane's two bits, then one ballot per word
     const int lane = threadIdx.x & 31;
-    const int64_t wbase = (l0 - 2 * lane) / 32;  // first word of this warp
+    const uint32_t v = (p0 ? 1u : 0u) | (p1 ? 2u : 0u);
+    const uint32_t v0 = __shfl_sync(0xffffffffu, v, lane >> 1);
+    const uint32_t v1 = __shfl_sync(0xffffffffu, v, 16 + (lane >> 1));
+    const uint32_t w0 = __ballot_sync(0xffffffffu, (v0 >> (lane & 1)) & 1u);
+    const uint32_t w1 = __ballot_sync(0xffffffffu, (v1 >> (lane & 1)) & 1u);
+    const int64_t wbase = c * 16 + 2 * (threadIdx.x >> 5);  // first word of this warp
     const int64_t nwords = (r + 31) / 32;
-    if (lane < 2 && wbase + lane < nwords) {
-      const uint32_t lo = lane ? (b0 >> 16) : b0, hi = lane ? (b1 >> 16) : b1;
-      perm[wbase + lane] = spread16(lo) | (spread16(hi) << 1);
-    }
+    if (lane < 2 && wbase + lane < nwords) perm[wbase + lane] = lane ? w1 : w0;
   }
 }
 
@@ -259,6 +252,7 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
       case 7: q[i] = sqrt_plain(x); break;
       case 8: q[i] = div_plain(x, rcp_plain(y)); break;
       case 9: q[i] = divide_small(x, rcp_plain(y), __activemask()); break;
+      case 10: q[i] = divide_gen(x, make_ndiv(y), __activemask()); break;
       default: q[i] = divide_sf<false, true>(x, make_divisor(y), __activemask()); break;
     }
   }
@@ -267,7 +261,7 @@ __global__ void debug_div_kernel(int64_t n, const double* a, const double* b, do
 
 extern "C" jsvd_status jsvd_debug_primitive(int32_t mode, int64_t n, const double* a,
                                             const double* b, double* q, void* stream) {
-  if (n < 0 || mode < 0 || mode > 9) return JSVD_EINVAL;
+  if (n < 0 || mode < 0 || mode > 10) return JSVD_EINVAL;
   if (n == 0) return JSVD_OK;
   jsvd::debug_div_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
                            static_cast<cudaStream_t>(stream)>>>(n, a, b, q, mode);

@@ -53,7 +53,7 @@ def test_division_full_range(seed):
         bad = _same(_run(mode, a, b), ref)
         assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
     nz = b != 0  # the EVD's specialised divisions require a nonzero divisor
-    for mode in (3, 4, 6):
+    for mode in (3, 4, 6, 10):
         bad = _same(_run(mode, a[nz], b[nz]), ref[nz])
         assert bad.size == 0, (mode, a[nz][bad[:4]], b[nz][bad[:4]])
 
@@ -73,7 +73,7 @@ def test_division_near_underflow_and_overflow():
     for x, y in ((a, b), (a2, b2), (hi, lo), (np.ldexp(np.ones(n), -1074), 1 + rng.random(n))):
         with np.errstate(all="ignore"):
             ref = x / y
-        for mode in (0, 3, 4, 6):
+        for mode in (0, 3, 4, 6, 10):
             bad = _same(_run(mode, x, y), ref)
             assert bad.size == 0, (mode, x[bad[:4]], y[bad[:4]])
 
@@ -90,7 +90,7 @@ def test_division_subnormal_ties():
             ys.append(np.full(odd.size, b))
     x, y = np.concatenate(xs), np.concatenate(ys)
     ref = x / y
-    for mode in (0, 3, 4, 6):
+    for mode in (0, 3, 4, 6, 10):
         bad = _same(_run(mode, x, y), ref)
         assert bad.size == 0, (mode, x[bad[:4]], y[bad[:4]])
 
@@ -113,7 +113,41 @@ def test_division_structured_significands():
     a, b = np.array(A), np.array(B)
     with np.errstate(all="ignore"):
         ref = a / b
-    for mode in (0, 1, 3, 4, 6):
+    for mode in (0, 1, 3, 4, 6, 10):
+        bad = _same(_run(mode, a, b), ref)
+        assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
+
+
+def test_division_double_rounding_midpoints():
+    # mode 10 rounds a subnormal result from the correctly rounded quotient Q
+    # of the normalised operands: wrong exactly when Q 2^k is a midpoint of the
+    # 2^-1074 grid while Q is inexact.  Build such cases: M a 53-bit
+    # significand whose low s bits are 10...0, Q = M 2^-52, b random, a =
+    # RN(Q b) 2^(eb - 1022 - s) over b 2^eb (so the s low bits of Q fall below
+    # the subnormal grid); keep the pairs where RN(a/b) at full precision is Q and
+    # the quotient is inexact (checked with exact rationals).  Both signs,
+    # divisors at several exponents.
+    from fractions import Fraction
+    rng = np.random.default_rng(17)
+    A, B = [], []
+    while len(A) < 4000:
+        s = int(rng.integers(1, 53))
+        M = (int(rng.integers(1 << 52, 1 << 53)) >> s << s) | (1 << (s - 1))
+        Q = M * 2.0 ** -52
+        b = float(1 + rng.random())
+        a = Q * b
+        if a / b != Q or Fraction(a) / Fraction(b) == Fraction(Q):
+            continue
+        eb = int(rng.integers(s, 1000))
+        E = eb - 1022 - s
+        sg = -1.0 if rng.random() < 0.5 else 1.0
+        sb = -1.0 if rng.random() < 0.3 else 1.0
+        A.append(sg * np.ldexp(a, E))
+        B.append(sb * np.ldexp(b, eb))
+    a, b = np.array(A), np.array(B)
+    ref = a / b
+    assert (np.abs(ref) < 2.0 ** -1022).all()
+    for mode in (0, 3, 10):
         bad = _same(_run(mode, a, b), ref)
         assert bad.size == 0, (mode, a[bad[:4]], b[bad[:4]])
 
