@@ -79,9 +79,8 @@ __device__ __forceinline__ void evd2_chunk(
     const uint32_t v1 = __shfl_sync(0xffffffffu, v, 16 + (lane >> 1));
     const uint32_t w0 = __ballot_sync(0xffffffffu, (v0 >> (lane & 1)) & 1u);
     const uint32_t w1 = __ballot_sync(0xffffffffu, (v1 >> (lane & 1)) & 1u);
-    const int64_t wbase = c * 16 + 2 * (threadIdx.x >> 5);  // first word of this warp
-    const int64_t nwords = (r + 31) / 32;
-    if (lane < 2 && wbase + lane < nwords) perm[wbase + lane] = lane ? w1 : w0;
+    const int64_t w = c * 16 + 2 * (threadIdx.x >> 5) + lane;  // word 2w + lane (lanes 0, 1)
+    if (lane < 2 && 32 * w < r) perm[w] = lane ? w1 : w0;
   }
 }
 

@@ -31,6 +31,7 @@ def _rand_doubles(rng, n):
     s = rng.integers(0, 2, n, dtype=np.uint64) << np.uint64(63)
     x = (s | (e << np.uint64(52)) | m).view(np.float64)
     x[rng.random(n) < 0.02] = 0.0
+    x[rng.random(n) < 0.01] = -0.0
     return x
 
 
