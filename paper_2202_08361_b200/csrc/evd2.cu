@@ -8,6 +8,8 @@
 // shuffles and two warp ballots.  No shared memory, no synchronisation.
 // Grid: one 256-thread CTA per 512 matrices (r = 2^26: 131072 CTAs, ~ 110
 // waves at 8 CTAs/SM).
+#include <cstdlib>
+
 #include "jsvd_dev.cuh"
 
 #include "jsvd_host.h"
@@ -91,12 +93,25 @@ __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
-    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm, int pf) {
   // programmatic dependent launch: the next grid in the stream may be scheduled
   // into the SMs this grid's last wave leaves free; every grid waits for its
   // predecessor's completion (and memory) before touching data
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (pf > 0 && threadIdx.x == 0) {
+    // L2 prefetch of the input chunk pf CTAs ahead (one bulk request per
+    // stream, issued by one thread through the TMA unit): HBM keeps streaming
+    // while the resident CTAs compute, and that chunk's loads hit L2
+    const int64_t cn = static_cast<int64_t>(blockIdx.x) + pf;
+    if ((cn + 1) * 512 <= r) {
+      const double* ps[4] = {a11, a22, are, aim};
+#pragma unroll
+      for (int k = 0; k < (CPLX ? 4 : 3); ++k)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;\n" ::"l"(ps[k] + cn * 512)
+                     : "memory");
+    }
+  }
   evd2_chunk<CPLX, TAN, NOBACK>(blockIdx.x, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
 }
 
@@ -106,10 +121,20 @@ __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
-    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
+    double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm, int pf) {
   if (MINB > 1) {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  }
+  if (pf > 0 && threadIdx.x == 0) {  // L2 prefetch pf CTAs ahead (as the vector kernel)
+    const int64_t cn = static_cast<int64_t>(blockIdx.x) + pf;
+    if ((cn + 1) * 256 <= r) {
+      const double* ps[4] = {a11, a22, are, aim};
+#pragma unroll
+      for (int k = 0; k < (CPLX ? 4 : 3); ++k)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 2048;\n" ::"l"(ps[k] + cn * 256)
+                     : "memory");
+    }
   }
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool in = l < r;
@@ -128,6 +153,21 @@ __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
     const uint32_t b = __ballot_sync(0xffffffffu, p);
     if ((threadIdx.x & 31) == 0 && l < r) perm[l / 32] = b;
   }
+}
+
+// L2 prefetch distance in CTAs: one wave of resident CTAs ahead (per_sm CTAs
+// per SM).  Measured, configs[1] (vector kernel, 4 per SM), 20 launches:
+// 0.942 -> 0.905 ms (two waves 0.906, four slower); configs[0] (scalar
+// kernel, 8 per SM): 12.8 -> 12.5 us (two or four waves: no gain).
+// JSVD_EVD_PF overrides (0: off).
+static int evd_prefetch_distance(int per_sm) {
+  const char* e = getenv("JSVD_EVD_PF");
+  if (e) return atoi(e);
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return per_sm * sms;
 }
 
 template <bool CPLX, bool TAN, bool NOBACK>
@@ -153,7 +193,7 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8>, r, a11, a22, re, im, l1, l2,
-                       c, sr, si, zeta, perm);
+                       c, sr, si, zeta, perm, evd_prefetch_distance(8));
     note_launch();
     return cudaGetLastError();
   }
@@ -171,11 +211,11 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK>, r, a11, a22, re, im, l1, l2, c,
-                       sr, si, zeta, perm);
+                       sr, si, zeta, perm, evd_prefetch_distance(4));
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm);
+        r, a11, a22, re, im, l1, l2, c, sr, si, zeta, perm, 0);
   }
   note_launch();
   return cudaGetLastError();
