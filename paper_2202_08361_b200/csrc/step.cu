@@ -44,6 +44,16 @@ __device__ __forceinline__ void cp_async_el(double* dst, const double* src, bool
                "r"(ok ? 8 : 0));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+// a hint: [ptr, ptr + bytes) into L2 (16-byte aligned interior, 1 MB requests)
+__device__ __forceinline__ void prefetch_l2(const void* ptr, int64_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
+  const uintptr_t e = (a + static_cast<uintptr_t>(bytes > 0 ? bytes : 0)) & ~uintptr_t(15);
+  a = (a + 15) & ~uintptr_t(15);
+  for (; a < e; a += (1u << 20)) {
+    const uint32_t sz = static_cast<uint32_t>(e - a < (1u << 20) ? e - a : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(sz) : "memory");
+  }
+}
 
 __device__ __forceinline__ double scalbn_el(double x, int n) { return scalbn_rn(x, n); }
 __device__ __forceinline__ double2 scalbn_el(double2 x, int n) {
@@ -99,6 +109,28 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
               static_cast<int>(P.step), static_cast<int>(pair), p, q);
   } else {
     strategy_pair(P.n, P.B, P.step, pair, p, q);
+  }
+  if (P.pf > 0 && threadIdx.x == 0) {
+    // L2 prefetch of the pair P.pf pairs ahead (one resident wave): this
+    // CTA's 1/CL of both columns, as bulk requests through the TMA unit
+    const int64_t pair2 = pair + P.pf;
+    if (pair2 < static_cast<int64_t>(gridDim.x / CL)) {
+      int p2, q2;
+      if (P.pairs) {
+        p2 = P.pairs[2 * pair2];
+        q2 = P.pairs[2 * pair2 + 1];
+      } else if (P.dist_nr > 0) {
+        dist_pair(static_cast<int>(P.n), static_cast<int>(P.B), P.dist_nr, P.dist_rank,
+                  static_cast<int>(P.step), static_cast<int>(pair2), p2, q2);
+      } else {
+        strategy_pair(P.n, P.B, P.step, pair2, p2, q2);
+      }
+      const int64_t rows = (P.m + CL - 1) / CL, r0 = crank * rows;
+      const int64_t nr = min(rows, P.m - r0);
+      const E* G0 = reinterpret_cast<const E*>(P.G);
+      prefetch_l2(G0 + static_cast<int64_t>(p2) * P.ldg + r0, nr * static_cast<int64_t>(sizeof(E)));
+      prefetch_l2(G0 + static_cast<int64_t>(q2) * P.ldg + r0, nr * static_cast<int64_t>(sizeof(E)));
+    }
   }
   const int L = crank * T + static_cast<int>(threadIdx.x);
   E* gp = reinterpret_cast<E*>(P.G) + static_cast<int64_t>(p) * P.ldg;
@@ -624,9 +656,26 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
   return e;
 }
 
+// L2 prefetch distance of the long-column step (shared-memory rows: G far
+// beyond L2): a quarter of the resident pairs (2 CTAs per SM, CL per pair).
+// Measured, configs[4] step: 2.145 ms without, 2.07 at 4 or 9 pairs ahead,
+// 2.09 at 13, 2.20 at 24, 2.35 at a full wave (37).  JSVD_STEP_PF overrides
+// (0: off).
+static int step_prefetch_distance(int CL) {
+  const char* e = getenv("JSVD_STEP_PF");
+  if (e) return atoi(e);
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return max(1, sms / (2 * CL));
+}
+
 template <bool CPLX>
-static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams& P,
+static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams& P0,
                                  cudaStream_t st) {
+  StepParams P = P0;
+  P.pf = g.NS ? step_prefetch_distance(g.CL) : 0;
   constexpr int NR = CPLX ? 8 : 16;
   using E = typename Elem<CPLX>::T;
   const int64_t grid = npairs * g.CL;
