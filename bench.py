@@ -333,7 +333,7 @@ class BatchedWorkload:
         self.st = torch.empty(self.b, dtype=torch.int32, device="cuda")
         self.tr = torch.empty(self.b, dtype=torch.int64, device="cuda")
         self.units_per_step = self.b
-        self.kernel = "batched_svd_kernel<1,4>"
+        self.kernel = "batched_fast_kernel<1,0>"
         self.l2_note = "2.1 GB of input per step > L2; A restored from a pristine copy before each step (untimed)"
 
     def prepare(self):
