@@ -297,9 +297,11 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
       bool bad = false;
       if (__any_sync(kFull, tr)) {
         double b11, b22, br, bi;
-        gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0, tr ? eq : 0.0,
-                  tr ? fq : 1.0, b11, b22, br, bi, kFull);
-        const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull);
+        const bool gf = gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0,
+                                  tr ? eq : 0.0, tr ? fq : 1.0, b11, b22, br, bi, kFull);
+        // |a21| = the test's |z| (a non-transformed lane's zero Grammian: 0)
+        const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull,
+                                                        !gf ? -1.0 : tr ? az : 0.0);
         if (tr) {
           P.c = o.c;
           P.C = o.sr;

@@ -471,7 +471,8 @@ __device__ __forceinline__ void gram(double zr, double zi, double e1, double f1,
 // per diagonal entry and leaves z unscaled; any lane outside it (exponents of
 // the two norms more than ~1022 apart) takes gram() in a uniform branch.
 // Same bits as gram() for every input it accepts (tested against the oracle).
-__device__ __forceinline__ void gram_fast(double zr, double zi, double e1, double f1, double e2,
+// returns true when this lane took the fast path (then br, bi = zr, zi)
+__device__ __forceinline__ bool gram_fast(double zr, double zi, double e1, double f1, double e2,
                                           double f2, double& a11, double& a22, double& br,
                                           double& bi, unsigned mask) {
   double f12 = div_plain(f1, rcp_plain(f2));
@@ -497,6 +498,7 @@ __device__ __forceinline__ void gram_fast(double zr, double zi, double e1, doubl
       bi = gi;
     }
   }
+  return fast;
 }
 
 // z = a / d for the dot's sums over d = fl(f_q f_p) in [1, 4) (Alg 3.1 line
