@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
       double gp = 1.0, gq = 1.0;
       if (!zp) eg_of(cs, spv, iep, gp);
       if (!zq) eg_of(cs, sqv, ieq, gq);
-      double arv = on ? P.ar : 0.0, aiv = on ? P.ai : 0.0;
+      // lanes without a pair divide a dummy 1 (a zero would send the whole
+      // warp into dot_div's tiny-dividend branch at every step)
+      double arv = on ? P.ar : 1.0, aiv = on ? P.ai : 1.0;
       if (!(zp || zq)) {  // the dot of G~ carries 2^(2cs - e_q - e_p) exactly
         const double f2 = pow2i(2 * cs - iep - ieq);
         arv *= f2;
