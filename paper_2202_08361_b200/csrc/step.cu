@@ -130,6 +130,12 @@ __global__ void __launch_bounds__(T, 2) step_kernel(const StepParams P) {
       const E* G0 = reinterpret_cast<const E*>(P.G);
       prefetch_l2(G0 + static_cast<int64_t>(p2) * P.ldg + r0, nr * static_cast<int64_t>(sizeof(E)));
       prefetch_l2(G0 + static_cast<int64_t>(q2) * P.ldg + r0, nr * static_cast<int64_t>(sizeof(E)));
+      if (P.V && P.pfv) {  // and its V columns (used if the pair transforms)
+        const int64_t vr = (P.n + CL - 1) / CL, v0 = crank * vr, vn = min(vr, P.n - v0);
+        const E* V0 = reinterpret_cast<const E*>(P.V);
+        prefetch_l2(V0 + static_cast<int64_t>(p2) * P.ldv + v0, vn * static_cast<int64_t>(sizeof(E)));
+        prefetch_l2(V0 + static_cast<int64_t>(q2) * P.ldv + v0, vn * static_cast<int64_t>(sizeof(E)));
+      }
     }
   }
   const int L = crank * T + static_cast<int>(threadIdx.x);
@@ -676,6 +682,11 @@ static cudaError_t launch_step_t(const Geo& g, int64_t npairs, const StepParams&
                                  cudaStream_t st) {
   StepParams P = P0;
   P.pf = g.NS ? step_prefetch_distance(g.CL) : 0;
+  {  // V too (2.065 -> 2.003 ms per configs[4] step when every pair
+     // transforms; a pair that then does not transform wastes its V bytes)
+    const char* e = getenv("JSVD_STEP_PFV");
+    P.pfv = P.pf > 0 && (e ? atoi(e) : 1);
+  }
   constexpr int NR = CPLX ? 8 : 16;
   using E = typename Elem<CPLX>::T;
   const int64_t grid = npairs * g.CL;

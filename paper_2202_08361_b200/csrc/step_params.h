@@ -15,6 +15,7 @@ struct StepParams {
   int dist_nr, dist_rank;  // dist_nr > 0: this rank's local pairs of the sharded ordering
   int fast;                // the scaled single-pass norms + dot, with fallback
   int pf;                  // L2 prefetch distance in pairs (0: off; set by launch_step)
+  int pfv;                 // prefetch the V columns too
   double tol;
   double* col_e;
   double* col_f;
