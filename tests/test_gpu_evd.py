@@ -120,6 +120,21 @@ def test_config2_full_size_bitwise(J):
     assert np.array_equal(bits, np.array([o["perm"] for o in one]))
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_l2_prefetch_is_invisible(J, monkeypatch, cplx):
+    # the EVD kernels' one-thread bulk L2 prefetch of the chunk pf CTAs ahead
+    # is a hint: off, the default (one resident wave) and a short distance
+    # give the oracle's bits on 2^20 matrices (2048 / 4096 CTAs)
+    arrs = synth.evd_cfg2(1 << 20) if cplx else synth.evd_cfg1(1 << 20)
+    ref = _ref(arrs, 0)
+    for pf in ("0", None, "7"):
+        if pf is None:
+            monkeypatch.delenv("JSVD_EVD_PF", raising=False)
+        else:
+            monkeypatch.setenv("JSVD_EVD_PF", pf)
+        _compare(_run(J, arrs, 0), ref, cplx)
+
+
 def test_north_star_tolerances_config2(J):
     # the stated EVD tolerances, on GPU output alone: ||U^H U - I||_F <= 8 eps
     # outside Eq. (5.1)-type inputs (R#11), eigenvalue sum/product invariants.

@@ -386,6 +386,27 @@ def test_sweep_step_long_V_bitwise(J, cplx, m, nv):
         assert out["mmax"].item() == ref["mmax"]
 
 
+@pytest.mark.parametrize("pf", ["0", "3"])
+def test_sweep_step_l2_prefetch_is_invisible(J, monkeypatch, pf):
+    # the long-column step's bulk L2 prefetch of the pair pf pairs ahead (its
+    # G columns and V columns) is a hint: 12 pairs of complex 32768-row
+    # columns, with and without it, bitwise against the oracle
+    monkeypatch.setenv("JSVD_STEP_PF", pf)
+    cplx, m, ncols = True, 32768, 24
+    rng = np.random.default_rng(29)
+    A = _scaled_input(rng, m, ncols, cplx, specials=False)
+    V = np.asfortranarray(np.eye(ncols) + 0j)
+    R = rspec(J, cplx, m)
+    G_ref, V_ref = A.copy(order="F"), V.copy(order="F")
+    g, v = colmajor_gpu(A), colmajor_gpu(V)
+    pairs = O.strategy_pairs(ncols, ncols, 0).astype(np.int32)
+    ref = O.step(G_ref, V_ref, pairs, R)
+    out = J.sweep_step(g, v, torch.from_numpy(pairs).cuda())
+    torch.cuda.synchronize()
+    assert int(out["t"].item()) == ref["t"]
+    assert bits_equal(to_np(g), G_ref) and bits_equal(to_np(v), V_ref)
+
+
 def test_config5_full_size_step_sampled_bitwise(J):
     # BASELINE configs[4] at full size (complex 32768 x 8192, 4.3 GB) in the
     # bench's launch configuration: one step of all 4096 pairs (block RR,
