@@ -22,11 +22,12 @@ namespace jsvd {
 template <bool CPLX>
 struct Chunk2 {
   double2 a11, a22, re, im;
-  __device__ __forceinline__ void load(int64_t r, int64_t tid, const double* __restrict__ p11,
+  template <typename I>
+  __device__ __forceinline__ void load(I r, I tid, const double* __restrict__ p11,
                                        const double* __restrict__ p22,
                                        const double* __restrict__ pre,
                                        const double* __restrict__ pim) {
-    const int64_t l0 = 2 * tid;
+    const I l0 = 2 * tid;
     a11 = a22 = re = im = make_double2(0.0, 0.0);
     if (l0 + 1 < r) {
       a11 = __ldcs(reinterpret_cast<const double2*>(p11) + tid);
@@ -44,14 +45,16 @@ struct Chunk2 {
 
 // one chunk: 512 consecutive matrices, 2 per thread (LDG.128 / STG.128 of
 // every SoA stream); the permutation words from two shuffles + two ballots
-template <bool CPLX, bool TAN, bool NOBACK>
+// I: the index type -- uint32_t when 2 r < 2^32 (one IMAD.WIDE.U32 per
+// stream address instead of 64-bit shift-and-add pairs), else int64_t
+template <bool CPLX, bool TAN, bool NOBACK, typename I>
 __device__ __forceinline__ void evd2_chunk(
-    int64_t c, int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
+    I c, I r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
     double* __restrict__ l2, double* __restrict__ cs, double* __restrict__ sr,
     double* __restrict__ si, int32_t* __restrict__ zeta, uint32_t* __restrict__ perm) {
-  const int64_t tid = c * 256 + threadIdx.x;
-  const int64_t l0 = 2 * tid;
+  const I tid = c * 256 + threadIdx.x;
+  const I l0 = 2 * tid;
   Chunk2<CPLX> x;
   x.load(r, tid, a11, a22, are, aim);
   const Evd2Out e0 = evd2<CPLX, TAN, NOBACK>(x.a11.x, x.a22.x, x.re.x, x.im.x, kFull);
@@ -81,14 +84,14 @@ __device__ __forceinline__ void evd2_chunk(
     const uint32_t v1 = __shfl_sync(0xffffffffu, v, 16 + (lane >> 1));
     const uint32_t w0 = __ballot_sync(0xffffffffu, (v0 >> (lane & 1)) & 1u);
     const uint32_t w1 = __ballot_sync(0xffffffffu, (v1 >> (lane & 1)) & 1u);
-    const int64_t w = c * 16 + 2 * (threadIdx.x >> 5) + lane;  // word 2w + lane (lanes 0, 1)
+    const I w = c * 16 + 2 * (threadIdx.x >> 5) + lane;  // word 2w + lane (lanes 0, 1)
     if (lane < 2 && 32 * w < r) perm[w] = lane ? w1 : w0;
   }
 }
 
 // one chunk per CTA (r/512 CTAs) at <= 64 registers: 4 CTAs per SM (a 5-CTA
 // bound spills and measured no better for configs[0], worse for configs[1])
-template <bool CPLX, bool TAN, bool NOBACK>
+template <bool CPLX, bool TAN, bool NOBACK, typename I>
 __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
@@ -112,11 +115,12 @@ __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
                      : "memory");
     }
   }
-  evd2_chunk<CPLX, TAN, NOBACK>(blockIdx.x, r, a11, a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
+  evd2_chunk<CPLX, TAN, NOBACK, I>(static_cast<I>(blockIdx.x), static_cast<I>(r), a11, a22, are, aim,
+                                   l1, l2, cs, sr, si, zeta, perm);
 }
 
-// scalar path for pointers that are only 8-byte aligned
-template <bool CPLX, bool TAN, bool NOBACK, int MINB = 1>
+// scalar path for pointers that are only 8-byte aligned (I as evd2_chunk)
+template <bool CPLX, bool TAN, bool NOBACK, int MINB = 1, typename I = int64_t>
 __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
@@ -136,8 +140,8 @@ __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
                      : "memory");
     }
   }
-  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in = l < r;
+  const I l = static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in = l < static_cast<I>(r);
   const Evd2Out e = evd2<CPLX, TAN, NOBACK>(in ? a11[l] : 0.0, in ? a22[l] : 0.0,
                                             in ? are[l] : 0.0, (CPLX && in) ? aim[l] : 0.0, kFull);
   const bool p = in && e.perm;
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
   }
   if (perm) {
     const uint32_t b = __ballot_sync(0xffffffffu, p);
-    if ((threadIdx.x & 31) == 0 && l < r) perm[l / 32] = b;
+    if ((threadIdx.x & 31) == 0 && in) perm[l / 32] = b;
   }
 }
 
@@ -192,8 +196,12 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8>, r, a11, a22, re, im, l1, l2,
-                       c, sr, si, zeta, perm, evd_prefetch_distance(8));
+    if (r < (int64_t(1) << 31))
+      cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8, uint32_t>, r, a11, a22, re, im,
+                         l1, l2, c, sr, si, zeta, perm, evd_prefetch_distance(8));
+    else
+      cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8, int64_t>, r, a11, a22, re, im,
+                         l1, l2, c, sr, si, zeta, perm, evd_prefetch_distance(8));
     note_launch();
     return cudaGetLastError();
   }
@@ -210,8 +218,12 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK>, r, a11, a22, re, im, l1, l2, c,
-                       sr, si, zeta, perm, evd_prefetch_distance(4));
+    if (r < (int64_t(1) << 31))
+      cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, uint32_t>, r, a11, a22, re, im, l1,
+                         l2, c, sr, si, zeta, perm, evd_prefetch_distance(4));
+    else
+      cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, int64_t>, r, a11, a22, re, im, l1,
+                         l2, c, sr, si, zeta, perm, evd_prefetch_distance(4));
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
