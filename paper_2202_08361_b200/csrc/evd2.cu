@@ -164,6 +164,13 @@ __global__ void __launch_bounds__(256, MINB) evd2_scalar_kernel(
 // 0.942 -> 0.905 ms (two waves 0.906, four slower); configs[0] (scalar
 // kernel, 8 per SM): 12.8 -> 12.5 us (two or four waves: no gain).
 // JSVD_EVD_PF overrides (0: off).
+// 32-bit indices for r < 2^31; JSVD_EVD_IDX64=1 forces the 64-bit kernels
+// (the form every r beyond 2^31 takes; the GPU tests compare both)
+static bool evd_idx32(int64_t r) {
+  const char* e = getenv("JSVD_EVD_IDX64");
+  return r < (int64_t(1) << 31) && !(e && atoi(e));
+}
+
 static int evd_prefetch_distance(int per_sm) {
   const char* e = getenv("JSVD_EVD_PF");
   if (e) return atoi(e);
@@ -196,7 +203,7 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (r < (int64_t(1) << 31))
+    if (evd_idx32(r))
       cudaLaunchKernelEx(&cfg, evd2_scalar_kernel<CPLX, TAN, NOBACK, 8, uint32_t>, r, a11, a22, re, im,
                          l1, l2, c, sr, si, zeta, perm, evd_prefetch_distance(8));
     else
@@ -218,7 +225,7 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (r < (int64_t(1) << 31))
+    if (evd_idx32(r))
       cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, uint32_t>, r, a11, a22, re, im, l1,
                          l2, c, sr, si, zeta, perm, evd_prefetch_distance(4));
     else

@@ -121,6 +121,15 @@ def test_config2_full_size_bitwise(J):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("r", [4097, 1 << 20])
+def test_64bit_index_kernels_bitwise(J, monkeypatch, cplx, r):
+    # the kernels every r >= 2^31 launches (64-bit indices), forced at small r
+    monkeypatch.setenv("JSVD_EVD_IDX64", "1")
+    arrs = synth.evd_cfg2(r) if cplx else synth.evd_cfg1(r)
+    _compare(_run(J, arrs, 0), _ref(arrs, 0), cplx)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
 def test_l2_prefetch_is_invisible(J, monkeypatch, cplx):
     # the EVD kernels' one-thread bulk L2 prefetch of the chunk pf CTAs ahead
     # is a hint: off, the default (one resident wave) and a short distance
