@@ -289,8 +289,6 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
         aiv *= f2;
       }
       const double fp = zp ? 1.0 : sqrt_plain(gp), fq = zq ? 1.0 : sqrt_plain(gq);
-      const double ep = zp ? -INFINITY : static_cast<double>(iep);
-      const double eq = zq ? -INFINITY : static_cast<double>(ieq);
       const Rcp d = rcp_plain(fq * fp);  // Alg 3.1 line 8
       const double zr = dot_div(arv, d, kFull);
       const double zi = CPLX ? dot_div(aiv, d, kFull) : 0.0;
@@ -299,8 +297,8 @@ __global__ void __launch_bounds__(kT, 6) batched_fast_kernel(
       bool bad = false;
       if (__any_sync(kFull, tr)) {
         double b11, b22, br, bi;
-        const bool gf = gram_fast(tr ? zr : 0.0, tr ? zi : 0.0, tr ? ep : 0.0, tr ? fp : 1.0,
-                                  tr ? eq : 0.0, tr ? fq : 1.0, b11, b22, br, bi, kFull);
+        const bool gf = gram_fast_i(tr ? zr : 0.0, tr ? zi : 0.0, tr ? iep : 0, tr ? fp : 1.0,
+                                    tr ? ieq : 0, tr ? fq : 1.0, b11, b22, br, bi, kFull);
         // |a21| = the test's |z| (a non-transformed lane's zero Grammian: 0)
         const Evd2Out o = evd2<CPLX, true, true, false>(b11, b22, br, bi, kFull,
                                                         !gf ? -1.0 : tr ? az : 0.0);

@@ -501,6 +501,37 @@ __device__ __forceinline__ bool gram_fast(double zr, double zi, double e1, doubl
   return fast;
 }
 
+// gram_fast with integral exponents passed as ints (no int <-> double
+// conversions on the caller's dependency chain; the same bits)
+__device__ __forceinline__ bool gram_fast_i(double zr, double zi, int e1, double f1, int e2,
+                                            double f2, double& a11, double& a22, double& br,
+                                            double& bi, unsigned mask) {
+  double f12 = div_plain(f1, rcp_plain(f2));
+  double f21 = div_plain(f2, rcp_plain(f1));
+  int e12 = e1 - e2, e21 = -e12;
+  const bool l12 = f12 < 1.0, l21 = f21 < 1.0;
+  e12 -= l12 ? 1 : 0;
+  e21 -= l21 ? 1 : 0;
+  f12 = l12 ? f12 * 2.0 : f12;
+  f21 = l21 ? f21 * 2.0 : f21;
+  const bool fast = max(e12, e21) <= kEtaHat && min(e12, e21) >= -1022;
+  a11 = f12 * pow2i(fast ? e12 : 0);
+  a22 = f21 * pow2i(fast ? e21 : 0);
+  br = zr;
+  bi = zi;
+  if (__any_sync(mask, !fast)) {
+    double g11, g22, gr, gi;
+    gram(zr, zi, static_cast<double>(e1), f1, static_cast<double>(e2), f2, g11, g22, gr, gi);
+    if (!fast) {
+      a11 = g11;
+      a22 = g22;
+      br = gr;
+      bi = gi;
+    }
+  }
+  return fast;
+}
+
 // z = a / d for the dot's sums over d = fl(f_q f_p) in [1, 4) (Alg 3.1 line
 // 8): the plain division when |a| >= 2^-968 (then the quotient is normal),
 // the general one in a uniform branch for tiny or zero sums
