@@ -45,6 +45,16 @@ std::mutex g_dbg_mu;
 int* g_dbg_flag[64] = {};
 }  // namespace
 
+int sm_count() {
+  static std::atomic<int> cache[64];  // 0: not queried yet
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0 && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    cache[dev].store(v, std::memory_order_relaxed);
+  return v;
+}
+
 bool debug_enabled() {
   const char* v = getenv("JSVD_DEBUG");
   return v && v[0] && v[0] != '0';

@@ -173,12 +173,7 @@ static bool evd_idx32(int64_t r) {
 
 static int evd_prefetch_distance(int per_sm) {
   const char* e = getenv("JSVD_EVD_PF");
-  if (e) return atoi(e);
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return 0;
-  return per_sm * sms;
+  return e ? atoi(e) : per_sm * sm_count();
 }
 
 template <bool CPLX, bool TAN, bool NOBACK>

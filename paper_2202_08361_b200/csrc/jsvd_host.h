@@ -14,6 +14,8 @@ bool debug_enabled();
 template <typename T>
 jsvd_status debug_check_finite(int64_t r, const T* a, const T* b, const T* c, const T* d,
                                cudaStream_t st);
+// the current device's SM count, queried once per device (0 on error)
+int sm_count();
 // batched.cu: the shape / dtype conditions of jsvd_gesvj_batched
 bool gesvj_batched_args_ok(jsvd_dtype dt, int64_t m, int64_t n);
 }  // namespace jsvd

@@ -670,11 +670,8 @@ static cudaError_t launch_cl(Kern k, int64_t grid, int T, int CL, size_t smem, c
 static int step_prefetch_distance(int CL) {
   const char* e = getenv("JSVD_STEP_PF");
   if (e) return atoi(e);
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return 0;
-  return max(1, sms / (2 * CL));
+  const int sms = sm_count();
+  return sms ? max(1, sms / (2 * CL)) : 0;
 }
 
 template <bool CPLX>
