@@ -230,6 +230,26 @@ def test_config3_full_size_step_bitwise(J):
         assert bits_equal(to_np(g), G) and bits_equal(to_np(v), V)
 
 
+def test_config3_full_size_gesvj_two_sweeps_bitwise(J):
+    # BASELINE configs[2] at full size through the driver the bench times
+    # (jsvd_gesvj, flat round-robin, the same call as bench.py's gesvj_r64)
+    # capped at two sweeps (2046 steps; the oracle takes seconds): status
+    # ENOCONV, G = U Sigma', V, Sigma' in column order, T per sweep and the
+    # final scale, all bitwise
+    A, _ = synth.svd_cfg3()
+    m, n = A.shape
+    R = rspec(J, False, m)
+    ref = O.gesvj(A, R, max_sweeps=2)
+    out = J.gesvj(colmajor_gpu(np.asfortranarray(A)), max_sweeps=2)
+    torch.cuda.synchronize()
+    assert out["status"] == ref["status"] == 1 and out["sweeps"] == ref["sweeps"] == 2
+    assert out["scale"] == ref["scale"] and list(out["tps"]) == list(ref["tps"])
+    for k in ("U", "V"):
+        assert bits_equal(to_np(out[k]), ref[k]), k
+    for k in ("sigma", "sigma_e", "sigma_f"):
+        assert bits_equal(out[k].cpu().numpy(), ref[k]), k
+
+
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("m,n", [(2, 2), (8, 6), (64, 32), (64, 16), (64, 30), (33, 32), (100, 40),
                                  (128, 64)])
