@@ -210,3 +210,40 @@ def test_dist_host_time_per_step():
         assert per_step_us <= 20.0, per_step_us
     finally:
         nd.close()
+
+
+def test_config5_full_size_sharded_equals_single_gpu():
+    # BASELINE configs[4] at full size (complex 32768 x 8192) through the
+    # sharded driver as the bench runs it (NCCL world of one, block moves
+    # through ncclSend/ncclRecv to self), one full sweep (8191 steps, 15
+    # block exchanges), against single-GPU jsvd_gesvj with the same ordering
+    # (B = 16) on the same matrix: the iterate G, V and Sigma' (status
+    # ENOCONV after the capped sweep) bitwise.  The oracle pins both paths on
+    # smaller matrices above; at this size the oracle would take hours.
+    import synth
+    import paper_2202_08361_b200 as J
+    from paper_2202_08361_b200.dist import NcclDist, local_columns
+    m, n, B = 32768, 8192, 16
+    A, _ = synth.svd_cfg5_torch(m, n, device="cuda")  # (m, n) column-major
+    cols = torch.from_numpy(local_columns(n, B, 0, 1)).cuda()
+    Al = A.T[cols].contiguous()  # (n, m): the rank's columns in slot order
+    ref = J.gesvj(A, nblocks=B, max_sweeps=1)
+    torch.cuda.synchronize()
+    nd = NcclDist.single(flags=J.DIST_SELF_P2P)
+    try:
+        V = torch.empty((n, n), dtype=torch.complex128, device="cuda")
+        work = torch.empty(J.gesvj_workspace(True, m, n, B, nd.dist), dtype=torch.uint8,
+                           device="cuda")
+        out = J.gesvj(Al.T, nblocks=B, max_sweeps=1, V=V.T, work=work, dist=nd.dist, n=n)
+        torch.cuda.synchronize()
+    finally:
+        nd.close()
+    assert out["status"] == ref["status"] == 1 and out["sweeps"] == ref["sweeps"] == 1
+    assert list(out["tps"]) == list(ref["tps"]) and out["scale"] == ref["scale"]
+    for k in ("sigma", "sigma_e", "sigma_f"):
+        assert torch.equal(out[k].view(torch.int64), ref[k].view(torch.int64)), k
+    # local column j is global column cols[j] (every block is home after a sweep)
+    assert torch.equal(torch.view_as_real(Al).view(torch.int64),
+                       torch.view_as_real(A.T[cols]).view(torch.int64))
+    assert torch.equal(torch.view_as_real(V[:, :]).view(torch.int64),
+                       torch.view_as_real(ref["V"].T[cols]).view(torch.int64))
