@@ -89,9 +89,10 @@ __device__ __forceinline__ void evd2_chunk(
   }
 }
 
-// one chunk per CTA (r/512 CTAs) at <= 64 registers: 4 CTAs per SM (a 5-CTA
-// bound spills and measured no better for configs[0], worse for configs[1])
-template <bool CPLX, bool TAN, bool NOBACK, typename I>
+// CPT consecutive chunks per CTA (r/512/CPT CTAs) at <= 64 registers: 4 CTAs
+// per SM (a 5-CTA bound spills and measured no better for configs[0], worse
+// for configs[1])
+template <bool CPLX, bool TAN, bool NOBACK, typename I, int CPT = 1>
 __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     int64_t r, const double* __restrict__ a11, const double* __restrict__ a22,
     const double* __restrict__ are, const double* __restrict__ aim, double* __restrict__ l1,
@@ -106,17 +107,20 @@ __global__ void __launch_bounds__(256, 4) evd2_vec2_kernel(
     // L2 prefetch of the input chunk pf CTAs ahead (one bulk request per
     // stream, issued by one thread through the TMA unit): HBM keeps streaming
     // while the resident CTAs compute, and that chunk's loads hit L2
-    const int64_t cn = static_cast<int64_t>(blockIdx.x) + pf;
-    if ((cn + 1) * 512 <= r) {
+    const int64_t cn = (static_cast<int64_t>(blockIdx.x) + pf) * CPT;
+    if ((cn + CPT) * 512 <= r) {
       const double* ps[4] = {a11, a22, are, aim};
 #pragma unroll
       for (int k = 0; k < (CPLX ? 4 : 3); ++k)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 4096;\n" ::"l"(ps[k] + cn * 512)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(ps[k] + cn * 512),
+                     "n"(4096 * CPT)
                      : "memory");
     }
   }
-  evd2_chunk<CPLX, TAN, NOBACK, I>(static_cast<I>(blockIdx.x), static_cast<I>(r), a11, a22, are, aim,
-                                   l1, l2, cs, sr, si, zeta, perm);
+#pragma unroll 1
+  for (int i = 0; i < CPT; ++i)
+    evd2_chunk<CPLX, TAN, NOBACK, I>(static_cast<I>(blockIdx.x) * CPT + i, static_cast<I>(r), a11,
+                                     a22, are, aim, l1, l2, cs, sr, si, zeta, perm);
 }
 
 // scalar path for pointers that are only 8-byte aligned (I as evd2_chunk)
@@ -208,11 +212,17 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     return cudaGetLastError();
   }
   if (vec) {
-    // one 512-matrix chunk per CTA: the measured-best shape for both configs
-    // (a persistent grid-stride variant was slower for configs[0] and [1])
+    // 512-matrix chunks, two consecutive ones per CTA (a persistent
+    // grid-stride variant was slower for configs[0] and [1], before the L2
+    // prefetch)
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
+    // two chunks per CTA, one after the other (the per-CTA fixed costs
+    // shared): configs[1] 0.893 -> 0.886 ms (20 launches), 0.994 -> 0.988 ms
+    // (200).  JSVD_EVD_CPT=1: one chunk per CTA.
+    const char* ce = getenv("JSVD_EVD_CPT");
+    const bool two = !(ce && atoi(ce) == 1);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(chunks));
+    cfg.gridDim = dim3(static_cast<unsigned>(two ? (chunks + 1) / 2 : chunks));
     cfg.blockDim = dim3(threads);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -220,12 +230,20 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (evd_idx32(r))
+    const bool i32 = evd_idx32(r);
+    const int pf = evd_prefetch_distance(4) / (two ? 2 : 1);  // the same distance in chunks
+    if (two && i32)
+      cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, uint32_t, 2>, r, a11, a22, re, im,
+                         l1, l2, c, sr, si, zeta, perm, pf);
+    else if (two)
+      cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, int64_t, 2>, r, a11, a22, re, im,
+                         l1, l2, c, sr, si, zeta, perm, pf);
+    else if (i32)
       cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, uint32_t>, r, a11, a22, re, im, l1,
-                         l2, c, sr, si, zeta, perm, evd_prefetch_distance(4));
+                         l2, c, sr, si, zeta, perm, pf);
     else
       cudaLaunchKernelEx(&cfg, evd2_vec2_kernel<CPLX, TAN, NOBACK, int64_t>, r, a11, a22, re, im, l1,
-                         l2, c, sr, si, zeta, perm, evd_prefetch_distance(4));
+                         l2, c, sr, si, zeta, perm, pf);
   } else {
     const int64_t blocks = (r + threads - 1) / threads;
     evd2_scalar_kernel<CPLX, TAN, NOBACK><<<static_cast<unsigned>(blocks), threads, 0, st>>>(

@@ -122,9 +122,22 @@ def test_config2_full_size_bitwise(J):
 
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("r", [4097, 1 << 20])
-def test_64bit_index_kernels_bitwise(J, monkeypatch, cplx, r):
-    # the kernels every r >= 2^31 launches (64-bit indices), forced at small r
+@pytest.mark.parametrize("cpt", ["1", "2"])
+def test_64bit_index_kernels_bitwise(J, monkeypatch, cplx, r, cpt):
+    # the kernels every r >= 2^31 launches (64-bit indices), forced at small r,
+    # with one or two 512-matrix chunks per CTA (JSVD_EVD_CPT)
     monkeypatch.setenv("JSVD_EVD_IDX64", "1")
+    monkeypatch.setenv("JSVD_EVD_CPT", cpt)
+    arrs = synth.evd_cfg2(r) if cplx else synth.evd_cfg1(r)
+    _compare(_run(J, arrs, 0), _ref(arrs, 0), cplx)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_one_chunk_per_cta_bitwise(J, monkeypatch, cplx):
+    # JSVD_EVD_CPT=1 (one 512-matrix chunk per CTA) against the oracle,
+    # ragged tail included
+    monkeypatch.setenv("JSVD_EVD_CPT", "1")
+    r = (1 << 18) + 777
     arrs = synth.evd_cfg2(r) if cplx else synth.evd_cfg1(r)
     _compare(_run(J, arrs, 0), _ref(arrs, 0), cplx)
 
