@@ -218,7 +218,7 @@ static cudaError_t launch_evd2(bool vec, int64_t r, const double* a11, const dou
     const int64_t chunks = (r + 2 * threads - 1) / (2 * threads);
     // two chunks per CTA, one after the other (the per-CTA fixed costs
     // shared): configs[1] 0.893 -> 0.886 ms (20 launches), 0.994 -> 0.988 ms
-    // (200).  JSVD_EVD_CPT=1: one chunk per CTA.
+    // (200); four per CTA: 0.896 / 0.994 ms.  JSVD_EVD_CPT=1: one chunk per CTA.
     const char* ce = getenv("JSVD_EVD_CPT");
     const bool two = !(ce && atoi(ce) == 1);
     cudaLaunchConfig_t cfg = {};
