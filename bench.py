@@ -900,6 +900,8 @@ def run_jsvd(args):
                     "hbm_peak_source": peak_src}
     if isinstance(wl, EvdWorkload) and wl.nsets > 1:  # the short configs[0] launch
         extra["size_matched_copy"] = size_matched_copy(wl, args.steps, peak)
+    if isinstance(wl, EvdWorkload) and wl.nsets == 1 and not wl.f32:
+        extra["streaming_copy"] = streaming_copy(wl, args.steps, peak, achieved)
     if isinstance(wl, GesvjWorkload):
         extra.update(extra_g)
         # capped (ENOCONV): sigma holds Sigma' in column order,
@@ -1071,6 +1073,39 @@ def size_matched_copy(wl, steps, peak):
     torch.cuda.empty_cache()
     return {"achieved": ach, "frac": ach / peak, "ms_per_step": ms,
             "what": "torch copy_ of the same bytes (read B/2 + write B/2), same buffer-set cycling"}
+
+
+def streaming_copy(wl, steps, peak, achieved):
+    """Context for the configs[1] line: the library's plain streaming copy
+    (jsvd_copy16: the EVD kernel's 16-byte streaming access pattern and
+    programmatic dependent launch) of the same bytes per step (read B/2 +
+    write B/2), K launches back to back in one CUDA graph as the EVD line
+    itself -- the rate a copy sustains over the same window."""
+    import torch
+    import paper_2202_08361_b200 as J
+    n16 = int(wl.bytes_per_step() // 2) // 16
+    src = torch.ones(2 * n16, dtype=torch.float64, device="cuda")
+    dst = torch.empty_like(src)
+    J.copy16(src, dst)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cap = torch.cuda.current_stream()
+        for _ in range(steps):
+            J.copy16(src, dst, stream=cap)
+    torch.cuda.synchronize()
+    graph_upload(g, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    ach = 2 * n16 * 16 / (ms / 1e3) / 1e9
+    del src, dst, g
+    torch.cuda.empty_cache()
+    return {"achieved": ach, "frac": ach / peak, "ms_per_step": ms, "evd_over_copy": achieved / ach,
+            "what": "jsvd_copy16 of the same bytes (read B/2 + write B/2), K launches in one graph"}
 
 
 def run_reference(args):

@@ -130,6 +130,8 @@ def lib():
         L.jsvd_norm_ef.argtypes = [ct.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
         L.jsvd_dgsscl.restype = ct.c_int
         L.jsvd_dgsscl.argtypes = [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
+        L.jsvd_copy16.restype = ct.c_int
+        L.jsvd_copy16.argtypes = [_i64, _vp, _vp, _vp]
         L.jsvd_fp64_peak.restype = ct.c_int
         L.jsvd_fp64_peak.argtypes = [_i32, _i64, _vp, ct.POINTER(_i64), _vp]
         L.jsvd_maxnorm.restype = ct.c_int
@@ -638,6 +640,18 @@ def dist_local_pairs(n, nblocks, rank, nranks, step):
     _check(lib().jsvd_dist_local_pairs(n, nblocks, rank, nranks, step, ct.cast(out, _vp)),
            "jsvd_dist_local_pairs")
     return [(out[2 * k], out[2 * k + 1]) for k in range(n // nranks // 2)]
+
+
+def copy16(src, dst, stream=None):
+    """jsvd_copy16: dst <- src (contiguous CUDA tensors of the same byte size,
+    a multiple of 16 bytes), the EVD kernel's streaming access pattern."""
+    if not (src.is_cuda and dst.is_cuda and src.is_contiguous() and dst.is_contiguous()):
+        raise ValueError("copy16: contiguous CUDA tensors")
+    nb = src.numel() * src.element_size()
+    if nb != dst.numel() * dst.element_size() or nb % 16:
+        raise ValueError("copy16: equal sizes, a multiple of 16 bytes")
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(lib().jsvd_copy16(nb // 16, _p(src), _p(dst), s.cuda_stream), "jsvd_copy16")
 
 
 def fp64_peak(iters=4096, blocks=None, stream=None):
