@@ -234,3 +234,15 @@ def test_divide_small_full_dividend_range():
         for y in (x, -x):
             bad = _same(_run(9, y, dd), y / dd)
             assert bad.size == 0, (dv, y[bad[:4]])
+
+
+def test_copy16_diagnostic():
+    # jsvd_copy16 (the bench's streaming-copy context line) copies exactly
+    import paper_2202_08361_b200 as J
+    src = torch.randn(1000002, dtype=torch.float64, device="cuda")
+    dst = torch.empty_like(src)
+    J.copy16(src, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(src, dst)
+    with pytest.raises(ValueError):
+        J.copy16(src[:3], dst[:3])
