@@ -554,8 +554,10 @@ class DistC64Workload:
         from paper_2202_08361_b200.dist import NcclDist, local_columns
         self.name, self.unit = name, "sweep-steps/s"
         self.desc = ("BASELINE configs[4]: complex fp64 Jacobi SVD of one 32768x8192 matrix, "
-                     f"column blocks (B=16) sharded over {world} GPU(s), NCCL block exchange "
-                     "inside libjsvd, the first 1024 sweep steps per call")
+                     f"column blocks (B=16) sharded over {world} GPU(s), "
+                     + ("NCCL block exchange inside libjsvd" if world > 1 else
+                        "one NCCL rank (block moves as device copies)")
+                     + ", the first 1024 sweep steps per call")
         A, _ = synth.svd_cfg5_torch()
         self.m, self.n = A.shape
         self.B = 16
